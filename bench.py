@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""bench.py — batched ptychographic objective+gradient throughput on B200.
+
+Headline workload (BASELINE.json configs[1] = "config 2"): complex64 object
+512x512, 64x64 complex probe, 29x29 serpentine raster at step 16 (841
+diffraction patterns), noiseless data.  One step = one objective+gradient
+evaluation (the reference's evaluate/phiDistance, objectives.cpp:52-118) over
+all 841 patterns; metric = diffraction patterns per second.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun, one rank per GPU): scan rows are split contiguously over
+ranks (weak in patterns per rank, fixed total = strong on the eval); each rank
+evaluates its shard and the gradient + misfit are summed with NCCL allreduce
+(the path's one real exchange step).
+
+--impl reference: the reference's own CPU path on the host cores (rank 0
+only): the patch-model restatement over the reference's compiled OpenMP
+kernels::fft2_inplace (oracle/_ref), same config/metric/unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+NPROC = os.cpu_count() or 1
+os.environ.setdefault("OMP_NUM_THREADS", str(NPROC))
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "diffraction patterns/sec per objective+gradient eval"
+UNIT = "patterns/s"
+FP32_LANES_PER_SM = 128
+N_SM = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--no-extras", action="store_true", help="skip V-cycle / PIE / CPU legs")
+    return ap.parse_args()
+
+
+def algorithmic(cfg, N):
+    """bytes and FLOPs of one objective+gradient evaluation."""
+    M, n = cfg.M, cfg.n
+    bd, bz = (4, 8) if cfg.precision == "c64" else (8, 16)
+    log2 = int(np.log2(M * M)) if M > 1 else 0
+    flops = N * (10 * M * M * log2 + 24 * M * M)
+    bytes_ = N * M * M * bd + 2 * n * n * bz
+    return bytes_, flops
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def load_traffic(key):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _reasons(self):
+        nv = self.nv
+        for fn in ("nvmlDeviceGetCurrentClocksEventReasons", "nvmlDeviceGetCurrentClocksThrottleReasons"):
+            if hasattr(nv, fn):
+                return getattr(nv, fn)(self.h)
+        return 0
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                bits = self._reasons()
+                for b, name in self.REASONS.items():
+                    if bits & b:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "samples": len(s),
+                "reasons": sorted(self.reasons - {"gpu_idle"})}
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_reference_eval_rate(cfg, obj, probe, pos, data, seconds: float):
+    """Reference CPU path: patch-model restatement (oracle/ptgo.c) whose 2-D FFTs
+    are the reference's own OpenMP kernels::fft2_inplace (kernels.cpp:126)."""
+    from oracle import ptgo
+    kind = "port"
+    if ptgo.has_reference():
+        ptgo.use_reference_fft(True)
+        kind = "reference"
+    ptgo.set_threads(NPROC)
+    cores = NPROC
+    p = ptgo.Problem(cfg.n, cfg.M, cfg.w, pos, data.astype(np.float64), probe.astype(np.complex128))
+    z = np.ones((cfg.n, cfg.n), np.complex128)
+    times = []
+    t_end = time.perf_counter() + seconds
+    while True:
+        t0 = time.perf_counter()
+        ptgo.evaluate(p, z)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() >= t_end and len(times) >= 1:
+            break
+    med = float(np.median(times))
+    ptgo.use_reference_fft(False) if kind == "reference" else None
+    sample = (f"{len(times)} full objective+gradient evals of {cfg.N} patterns (median {med * 1e3:.1f} ms); "
+              + ("patch-model restatement (oracle/ptgo.c) over the reference's compiled "
+                 f"kernels::fft2_inplace, scan positions spread over {cores} OpenMP threads "
+                 "(results identical to the serial loop)" if kind == "reference" else
+                 f"oracle port, pattern-parallel OpenMP ({cores} threads)"))
+    return cfg.N / med, cores, kind, sample, med
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    from paper_1810_05628_b200 import synth
+    from oracle import ptgo
+    cfg = synth.CONFIGS[args.config]
+    obj, probe, pos = synth.make_inputs(cfg)
+    if cfg.precision == "c64":
+        obj = obj.astype(np.complex64).astype(np.complex128)
+        probe = probe.astype(np.complex64).astype(np.complex128)
+    data = ptgo.simulate(cfg.n, cfg.M, cfg.w, pos, obj, probe)
+    if cfg.photons:
+        data = synth.poisson(data, cfg.photons)
+    if cfg.precision == "c64":
+        data = data.astype(np.float32).astype(np.float64)
+    kind = "port"
+    if ptgo.has_reference():
+        ptgo.use_reference_fft(True)
+        kind = "reference"
+    ptgo.set_threads(NPROC)
+    cores = NPROC
+    p = ptgo.Problem(cfg.n, cfg.M, cfg.w, pos, data, probe)
+    z = np.ones((cfg.n, cfg.n), np.complex128)
+    for _ in range(max(args.warmup, 0)):
+        ptgo.evaluate(p, z)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ptgo.evaluate(p, z)
+    dt = time.perf_counter() - t0
+    value = cfg.N * args.steps / dt
+    sample = (f"{args.steps} full evals x {cfg.N} patterns, "
+              + (f"patch-model restatement over the reference's compiled kernels::fft2_inplace, "
+                 f"positions over {cores} OpenMP threads" if kind == "reference"
+                 else "oracle port, pattern-parallel"))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": cfg.describe(), "global_batch": cfg.N, "parallelism": "cpu"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1810_05628_b200 import Hierarchy, Plan, synth
+
+    cfg = synth.CONFIGS[args.config]
+    obj, probe, pos = synth.make_inputs(cfg)
+    rows_per = -(-cfg.steps // world)
+    lo, hi = min(rank * rows_per, cfg.steps) * cfg.steps, min((rank + 1) * rows_per, cfg.steps) * cfg.steps
+    pos_shard = pos[lo:hi]
+    Nr = pos_shard.shape[0]
+
+    cdt = torch.complex64 if cfg.precision == "c64" else torch.complex128
+    # a real (non-legacy) stream shared by torch and libptg so CUDA events see our kernels
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    plan = Plan(cfg.n, cfg.M, cfg.w, pos_shard, None, probe, precision=cfg.precision, device=local)
+    plan.set_stream(stream.cuda_stream)
+    # data: our GPU forward operator (forward.cpp:40-54 restated), + Poisson if configured
+    host_data = plan.simulate(obj, copy_out=bool(cfg.photons))
+    if cfg.photons:
+        plan.set_data(synth.poisson(host_data, cfg.photons, seed=4 + rank))
+    z = torch.ones(cfg.n, cfg.n, dtype=cdt, device="cuda")
+    grad = torch.empty_like(z)
+    val = torch.zeros(4, dtype=torch.float64, device="cuda")
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+
+    def step():
+        plan.evaluate_device(z, grad, value_dev=val, sync_value=False)
+        if dist is not None:
+            dist.all_reduce(torch.view_as_real(grad))
+            dist.all_reduce(val[:1])
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    plan.set_timing(True)
+    plan.get_timing()
+    l0 = plan.launch_count
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    sampler = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ
+                           else local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    for i in range(args.steps):
+        flush.zero_()                      # evict L2 between timed iterations (not timed)
+        starts[i].record(stream)
+        step()
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clocks = sampler.stop()
+    t_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    frame_ms, frame_n, gather_ms, gather_n = plan.get_timing()
+    plan.set_timing(False)
+    launches = plan.launch_count - l0
+    if dist is not None:
+        t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+
+    total_patterns = cfg.N
+    value = total_patterns * args.steps / (t_ms / 1e3)
+    ms_per_step = t_ms / args.steps
+
+    # roofline of the dominant kernel (frame kernel), live CUDA-event durations
+    peaks, peak_src = load_peaks()
+    B, F = algorithmic(cfg, Nr)
+    avg_frame_s = (frame_ms / max(frame_n, 1)) / 1e3
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved_gbs = B / avg_frame_s / 1e9
+    sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = N_SM * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    achieved_tf = F / avg_frame_s / 1e12
+    traffic = load_traffic(f"config{cfg.cid}_frame_kernel")
+    roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved_gbs / hbm_peak, "traffic": traffic,
+                "kernel": f"frame_kernel<float,{cfg.M}> (one CTA per scan position)",
+                "algorithmic_bytes_per_launch": B, "avg_launch_us": avg_frame_s * 1e6,
+                "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"}
+    roofline_fp32 = {"bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
+                     "frac": achieved_tf / fp32_peak, "algorithmic_flops_per_launch": F,
+                     "convention": "F(M)=10 M^2 log2(M^2) + 24 M^2 per pattern (SURVEY 8d)",
+                     "peak_source": f"nominal 148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (no measured FP32 figure)"}
+    eval_share = {"frame_kernel_ms": frame_ms / max(args.steps, 1), "gather_ms": gather_ms / max(args.steps, 1),
+                  "frame_share_of_step": frame_ms / max(t_ms, 1e-12)}
+
+    # ---- e2e through the public host API: pinned host z in, value + grad out
+    e2e = None
+    zh = torch.ones(cfg.n, cfg.n, dtype=torch.complex128).pin_memory().numpy()
+    gh = torch.empty(cfg.n, cfg.n, dtype=torch.complex128).pin_memory().numpy()
+    h2d = zh.nbytes
+    d2h = gh.nbytes + 8
+    for _ in range(2):
+        plan.evaluate(zh, out=gh) if world == 1 else None
+    if world == 1:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            plan.evaluate(zh, out=gh)
+        e2e_s = time.perf_counter() - t0
+    else:
+        zt = torch.empty_like(z)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            zt.copy_(torch.from_numpy(zh).to(cdt), non_blocking=False)
+            plan.evaluate_device(zt, grad, value_dev=val, sync_value=False)
+            dist.all_reduce(torch.view_as_real(grad))
+            dist.all_reduce(val[:1])
+            torch.from_numpy(gh).copy_(grad.to(torch.complex128))
+            float(val[0].item())
+        e2e_s = time.perf_counter() - t0
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e = {"value": total_patterns * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s / args.steps * 1e3,
+           "api": "Plan.evaluate (ptg_eval): pinned complex128 z in, value + complex128 gradient out"}
+
+    extras = {}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_extras:
+        # PIE sweep (solvers.cpp:229-265), config-2 geometry
+        try:
+            zp = torch.ones_like(z)
+            plan.pie_sweep_device(zp)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(3):
+                plan.pie_sweep_device(zp)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            extras["pie_sweep_ms"] = e0.elapsed_time(e1) / 3
+        except Exception as ex:   # noqa: BLE001
+            extras["pie_sweep_error"] = str(ex)
+        # MG/OPT V-cycle on config 3 (3 levels, M=128, jittered raster)
+        try:
+            c3 = synth.CONFIGS[3]
+            o3, p3, s3 = synth.make_inputs(c3)
+            plan3 = Plan(c3.n, c3.M, c3.w, s3, None, p3, precision=c3.precision, device=local)
+            plan3.set_stream(stream.cuda_stream)
+            plan3.simulate(o3, copy_out=False)
+            h3 = Hierarchy(plan3, c3.depth)
+            z3 = torch.ones(c3.n, c3.n, dtype=torch.complex64, device="cuda")
+            g3 = torch.empty_like(z3)
+            v3 = plan3.evaluate_device(z3, g3)
+            v3, _, _ = h3.cycle_device(z3, g3, v3)   # warm-up cycle
+            torch.cuda.synchronize()
+            cyc = []
+            per = None
+            for _ in range(3):
+                t0 = time.perf_counter()
+                v3, wt, per = h3.cycle_device(z3, g3, v3)
+                torch.cuda.synchronize()
+                cyc.append((time.perf_counter() - t0) * 1e3)
+            extras["vcycle"] = {"config": 3, "levels": c3.depth, "ms": float(np.median(cyc)),
+                                "weighted_evals_per_cycle": wt, "evals_per_level_per_cycle": per,
+                                "value_after": v3}
+            h3.close()
+            plan3.close()
+        except Exception as ex:   # noqa: BLE001
+            extras["vcycle_error"] = str(ex)
+        # CPU baseline on a bounded sample of the same workload
+        try:
+            host_data = plan.simulate(obj, copy_out=True)
+            rate, cores, kind, sample, _ = cpu_reference_eval_rate(
+                cfg, obj.astype(np.complex64).astype(np.complex128) if cfg.precision == "c64" else obj,
+                probe, pos, host_data, args.cpu_seconds)
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+        except Exception as ex:   # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": NPROC, "kind": "reference", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32" if cfg.precision == "c64" else "f64",
+                "data": "synthetic (seeded smooth object, Gaussian x quadratic-phase probe, data by our GPU forward operator)",
+                "config": {"workload": cfg.describe(), "global_batch": cfg.N, "patterns_per_rank": Nr,
+                           "parallelism": f"scan-row sharding x{world} + NCCL allreduce" if world > 1 else "single GPU",
+                           "l2": "flushed between timed steps (512 MiB write)"},
+                "roofline": roofline, "roofline_fp32": roofline_fp32, "step_breakdown": eval_share,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
+        line.update(extras)
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

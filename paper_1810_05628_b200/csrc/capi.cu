@@ -1,0 +1,491 @@
+// capi.cu — extern "C" boundary of libptg (include/ptg.h).
+//
+// Every entry point converts ptg::Status exceptions (and std::bad_alloc,
+// CUDA errors) into an int status and a thread-local message, mirroring the
+// reference's exception hierarchy (/root/reference/proj/include/ptycho/
+// errors.hpp:12-43) so a C++ shim can re-throw the matching type.
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <new>
+#include <string>
+
+#include "plan.cuh"
+#include "solvers.cuh"
+#include "transfer.cuh"
+
+struct ptg_plan {
+    std::unique_ptr<ptg::Plan> p;
+};
+struct ptg_hier {
+    std::unique_ptr<ptg::Hier> h;
+    ptg_plan* fine;
+    std::vector<ptg_plan> views;   // non-owning plan handles for coarse levels
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return PTG_OK;
+    } catch (const ptg::Status& s) {
+        g_err = s.what();
+        return s.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of host memory";
+        return PTG_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return PTG_ERR_INTERNAL;
+    }
+}
+
+ptg::Plan& P(ptg_plan* p) {
+    if (!p || !p->p) ptg::raise(PTG_ERR_CONFIG, "objective is not bound to geometry/data (null plan)");
+    PTG_CUDA(cudaSetDevice(p->p->device));
+    return *p->p;
+}
+
+void fill_report(ptg_report* rep, const ptg::Counter& c, double value, int reason, int hist_len) {
+    if (!rep) return;
+    rep->final_value = value;
+    rep->weighted = c.weighted;
+    for (int i = 0; i < 16; ++i) rep->per_level[i] = c.per_level[i];
+    rep->reason = reason;
+    rep->hist_len = hist_len;
+}
+
+int copy_hist(const std::vector<ptg_hist>& h, ptg_hist* out, int cap) {
+    const int n = (int)h.size();
+    if (out)
+        for (int i = 0; i < n && i < cap; ++i) out[i] = h[i];
+    return n;
+}
+}  // namespace
+
+namespace {
+template <class F>
+void with_device_buffers(size_t in_bytes, const void* in, size_t out_bytes, void* out, F&& f) {
+    ptg::DevMem a, b;
+    a.alloc(in_bytes);
+    b.alloc(out_bytes);
+    PTG_CUDA(cudaMemcpy(a.p, in, in_bytes, cudaMemcpyHostToDevice));
+    f(a.p, b.p);
+    PTG_CUDA(cudaDeviceSynchronize());
+    PTG_CUDA(cudaMemcpy(out, b.p, out_bytes, cudaMemcpyDeviceToHost));
+}
+}  // namespace
+
+static void sync_streams(ptg::Hier& h) {
+    for (auto* l : h.levels) l->stream = h.fine->stream;
+}
+
+extern "C" {
+
+const char* ptg_last_error(void) { return g_err.c_str(); }
+
+int ptg_version(void) { return 1; }
+
+int ptg_device_count(int* count) {
+    return guard([&] {
+        int c = 0;
+        cudaError_t e = cudaGetDeviceCount(&c);
+        if (e != cudaSuccess) c = 0;
+        *count = c;
+    });
+}
+
+void ptg_solver_cfg_default(ptg_solver_cfg* c) {
+    c->max_iters = 100;
+    c->grad_tol_rel = 0.0;
+    c->grad_tol_abs = 1e-13;
+    c->lbfgs_memory = 25;
+    c->linesearch_max = 50;
+    c->max_weighted = std::numeric_limits<double>::infinity();
+}
+
+void ptg_mg_cfg_default(ptg_mg_cfg* c) {
+    c->k1 = 1;
+    c->k2 = 1;
+    c->coarsest_max_iters = 0;
+    c->coarsest_grad_tol_rel = 1e-4;
+    c->intermediate_grad_tol_rel = 1e-3;
+    c->lbfgs_memory = 25;
+    c->linesearch_max = 50;
+    c->grad_tol_abs = 1e-13;
+}
+
+void ptg_driver_cfg_default(ptg_driver_cfg* c) {
+    c->budget = 100.0;
+    c->grad_tol_rel = 0.0;
+    c->grad_tol_abs = 1e-13;
+    c->max_cycles = 1000000;
+}
+
+int ptg_plan_create(const ptg_plan_desc* desc, ptg_plan** out) {
+    return guard([&] {
+        if (!desc || !out) ptg::raise(PTG_ERR_CONFIG, "null argument");
+        *out = nullptr;
+        auto h = new ptg_plan;
+        try {
+            h->p = ptg::plan_create(*desc);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int ptg_plan_destroy(ptg_plan* plan) {
+    return guard([&] {
+        if (!plan) return;
+        if (plan->p) {
+            cudaSetDevice(plan->p->device);
+            cudaStreamSynchronize(plan->p->stream);
+            cudaStream_t own = plan->p->own_stream;
+            plan->p.reset();
+            if (own) cudaStreamDestroy(own);
+        }
+        delete plan;
+    });
+}
+
+int ptg_plan_set_stream(ptg_plan* plan, void* stream) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        p.stream = stream ? static_cast<cudaStream_t>(stream) : p.own_stream;
+    });
+}
+
+int ptg_plan_set_data(ptg_plan* plan, const void* host_data, int dtype) {
+    return guard([&] { ptg::plan_set_data_host(P(plan), host_data, dtype); });
+}
+
+int ptg_plan_set_data_device(ptg_plan* plan, const void* dev_data, int dtype) {
+    return guard([&] { ptg::plan_set_data_device(P(plan), dev_data, dtype); });
+}
+
+int ptg_plan_info(const ptg_plan* plan, int* n, int* M, int* w, int* N, int* precision,
+                  size_t* device_bytes) {
+    return guard([&] {
+        if (!plan || !plan->p) ptg::raise(PTG_ERR_CONFIG, "null plan");
+        const ptg::Plan& p = *plan->p;
+        if (n) *n = p.n;
+        if (M) *M = p.M;
+        if (w) *w = p.w;
+        if (N) *N = p.N;
+        if (precision) *precision = p.prec;
+        if (device_bytes) *device_bytes = p.device_bytes();
+    });
+}
+
+int ptg_plan_launch_count(const ptg_plan* plan, int64_t* count) {
+    return guard([&] {
+        if (!plan || !plan->p) ptg::raise(PTG_ERR_CONFIG, "null plan");
+        *count = plan->p->launches;
+    });
+}
+
+int ptg_plan_set_timing(ptg_plan* plan, int enable) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        p.timing = enable != 0;
+        p.ev_used = 0;
+    });
+}
+
+int ptg_plan_get_timing(ptg_plan* plan, double* frame_ms, int64_t* frame_launches,
+                        double* gather_ms, int64_t* gather_launches) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        double ms[2];
+        int64_t cnt[2];
+        p.timing_collect(ms, cnt);
+        if (frame_ms) *frame_ms = ms[0];
+        if (frame_launches) *frame_launches = cnt[0];
+        if (gather_ms) *gather_ms = ms[1];
+        if (gather_launches) *gather_launches = cnt[1];
+    });
+}
+
+int ptg_eval(ptg_plan* plan, int metric, const double* z, const double* v, double* value,
+             double* grad) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        const size_t bytes = p.nn() * p.celem();
+        p.zbuf.ensure(bytes);
+        p.gbuf.ensure(bytes);
+        ptg::plan_upload_c128(p, z, p.zbuf.p);
+        if (v) {
+            p.vbuf.ensure(bytes);
+            ptg::plan_upload_c128(p, v, p.vbuf.p);
+        }
+        ptg::plan_eval(p, metric, p.zbuf.p, v ? p.vbuf.p : nullptr, p.gbuf.p, p.value.as<double>());
+        if (grad) ptg::plan_download_c128(p, p.gbuf.p, grad);
+        const double val = ptg::plan_read_scalar(p, p.value.as<double>());
+        if (value) *value = val;
+    });
+}
+
+int ptg_eval_device(ptg_plan* plan, int metric, const void* z, const void* v, void* grad,
+                    double* value_dev, double* value_host) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        double* vd = value_dev ? value_dev : p.value.as<double>();
+        ptg::plan_eval(p, metric, z, v, grad, vd);
+        if (value_host) *value_host = ptg::plan_read_scalar(p, vd);
+    });
+}
+
+int ptg_project_modulus(ptg_plan* plan, const double* z, int k, double* frame) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        p.zbuf.ensure(p.nn() * p.celem());
+        ptg::plan_upload_c128(p, z, p.zbuf.p);
+        ptg::DevMem out;
+        out.alloc(p.MM() * p.celem());
+        ptg::plan_project(p, p.zbuf.p, k, out.p);
+        ptg::DevMem out64;
+        out64.alloc(p.MM() * 16);
+        {
+            ptg::LaunchScope ls(p);
+            ptg::dev_to_c128(p.prec, out64.as<double>(), out.p, p.MM(), p.stream);
+        }
+        PTG_CUDA(cudaMemcpyAsync(frame, out64.p, p.MM() * 16, cudaMemcpyDeviceToHost, p.stream));
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+    });
+}
+
+int ptg_simulate(ptg_plan* plan, const double* z, double* data_out) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        p.zbuf.ensure(p.nn() * p.celem());
+        ptg::plan_upload_c128(p, z, p.zbuf.p);
+        ptg::plan_simulate(p, p.zbuf.p);
+        if (data_out) {
+            const size_t len = (size_t)p.N * p.MM();
+            ptg::DevMem d64;
+            d64.alloc(std::max<size_t>(1, len) * 8);
+            {
+                ptg::LaunchScope ls(p);
+                ptg::dev_real_convert(PTG_C128, d64.p, p.prec == PTG_C64 ? PTG_F32 : PTG_F64, p.inten.p, len, p.stream);
+            }
+            PTG_CUDA(cudaMemcpyAsync(data_out, d64.p, len * 8, cudaMemcpyDeviceToHost, p.stream));
+        }
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+    });
+}
+
+int ptg_simulate_device(ptg_plan* plan, const void* z) {
+    return guard([&] { ptg::plan_simulate(P(plan), z); });
+}
+
+int ptg_pie(ptg_plan* plan, double* z, double gamma, int sweeps, double max_weighted,
+            double* final_value, ptg_hist* hist, int hist_cap, int* hist_len, double* weighted,
+            int* reason) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        if (gamma < 0.0) ptg::raise(PTG_ERR_CONFIG, "pie: gamma must be non-negative");
+        const size_t len = p.nn();
+        ptg::DVec zd(p, len), gd(p, len);
+        ptg::plan_upload_c128(p, z, zd.p);
+        std::vector<ptg_hist> h;
+        ptg::Counter ctr;
+        auto diag = [&]() {   // uncounted diagnostic evaluation (solvers.cpp:238,254,263)
+            ptg::plan_eval(p, PTG_DISTANCE, zd.p, nullptr, gd.p, p.value.as<double>());
+            const double val = ptg::plan_read_scalar(p, p.value.as<double>());
+            return val;
+        };
+        double val = diag();
+        h.push_back({ctr.weighted, val, std::sqrt(ptg::plan_dot(p, gd.p, gd.p, len))});
+        int rsn = PTG_STOP_MAXITERS;
+        for (int sweep = 1; sweep <= sweeps; ++sweep) {
+            ptg::plan_pie_sweep(p, zd.p, gamma);
+            if (ptg::plan_nonfinite(p, zd.p, len)) ptg::raise(PTG_ERR_NUMERIC, "non-finite iterate in pie");
+            ctr.record(0, 1.0);   // one sweep = one fine-level evaluation
+            val = diag();
+            h.push_back({ctr.weighted, val, std::sqrt(ptg::plan_dot(p, gd.p, gd.p, len))});
+            if (ctr.weighted >= max_weighted) {
+                rsn = PTG_STOP_BUDGET;
+                break;
+            }
+        }
+        val = diag();
+        ptg::plan_download_c128(p, zd.p, z);
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+        if (final_value) *final_value = val;
+        const int n = copy_hist(h, hist, hist_cap);
+        if (hist_len) *hist_len = n;
+        if (weighted) *weighted = ctr.weighted;
+        if (reason) *reason = rsn;
+    });
+}
+
+int ptg_pie_sweep_device(ptg_plan* plan, void* z, double gamma) {
+    return guard([&] { ptg::plan_pie_sweep(P(plan), z, gamma); });
+}
+
+// ------------------------------------------------------------- transfers
+
+int ptg_restrict_field(const double* fine, int n, double* coarse) {
+    return guard([&] {
+        if (n < 2 || n % 2 != 0)
+            ptg::raise(PTG_ERR_GEOMETRY, "restrictField: grid side must be even and >= 2, got " + std::to_string(n));
+        const size_t fb = (size_t)n * n * 16, cb = (size_t)(n / 2) * (n / 2) * 16;
+        with_device_buffers(fb, fine, cb, coarse, [&](void* a, void* b) {
+            ptg::dev_restrict_field(PTG_C128, a, n, b, nullptr);
+        });
+    });
+}
+
+int ptg_prolong_field(const double* coarse, int nH, double* fine) {
+    return guard([&] {
+        if (nH < 1) ptg::raise(PTG_ERR_GEOMETRY, "prolongField: empty grid");
+        const size_t cb = (size_t)nH * nH * 16, fb = (size_t)4 * nH * nH * 16;
+        with_device_buffers(cb, coarse, fb, fine, [&](void* a, void* b) {
+            ptg::dev_prolong_field(PTG_C128, a, nH, b, nullptr);
+        });
+    });
+}
+
+int ptg_restrict_data(const double* fine, int N, int M, double* coarse) {
+    return guard([&] {
+        if (M < 4 || M % 4 != 0) ptg::raise(PTG_ERR_GEOMETRY, "restrictData: grid side must be a multiple of 4");
+        if (N <= 0) return;
+        const size_t fb = (size_t)N * M * M * 8, cb = (size_t)N * (M / 2) * (M / 2) * 8;
+        with_device_buffers(fb, fine, cb, coarse, [&](void* a, void* b) {
+            ptg::dev_restrict_data(PTG_F64, a, N, M, b, 1.0 / 16.0, nullptr);
+        });
+    });
+}
+
+int ptg_restrict_field_device(int precision, const void* fine, int n, void* coarse, void* stream) {
+    return guard([&] { ptg::dev_restrict_field(precision, fine, n, coarse, (cudaStream_t)stream); });
+}
+
+int ptg_prolong_field_device(int precision, const void* coarse, int nH, void* fine, void* stream) {
+    return guard([&] { ptg::dev_prolong_field(precision, coarse, nH, fine, (cudaStream_t)stream); });
+}
+
+int ptg_restrict_data_device(int dtype, const void* fine, int N, int M, void* coarse, void* stream) {
+    return guard([&] { ptg::dev_restrict_data(dtype, fine, N, M, coarse, 1.0 / 16.0, (cudaStream_t)stream); });
+}
+
+// ---------------------------------------------------------------- solvers
+int ptg_lbfgs(ptg_plan* plan, int metric, const double* v, const double* z0,
+              const ptg_solver_cfg* cfg, double* z_out, double* grad_out, ptg_report* rep,
+              ptg_hist* hist, int hist_cap) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        ptg_solver_cfg c;
+        if (cfg) c = *cfg;
+        else ptg_solver_cfg_default(&c);
+        const size_t len = p.nn();
+        ptg::DVec zd(p, len), vd, zo(p, len), go(p, len);
+        ptg::plan_upload_c128(p, z0, zd.p);
+        if (v) {
+            vd.alloc(p, len);
+            ptg::plan_upload_c128(p, v, vd.p);
+        }
+        ptg::DObj obj;
+        obj.plan = &p;
+        obj.metric = metric;
+        obj.v = v ? vd.p : nullptr;
+        ptg::Counter ctr;
+        std::vector<ptg_hist> h;
+        ptg::SolveOut o = ptg::d_lbfgs(obj, zd.p, c, ctr, nullptr, nullptr, zo.p, go.p, &h);
+        if (z_out) ptg::plan_download_c128(p, zo.p, z_out);
+        if (grad_out) ptg::plan_download_c128(p, go.p, grad_out);
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+        fill_report(rep, ctr, o.value, o.reason, copy_hist(h, hist, hist_cap));
+    });
+}
+
+int ptg_hier_create(ptg_plan* fine, int metric, int depth, const ptg_mg_cfg* opt, ptg_hier** out) {
+    return guard([&] {
+        ptg::Plan& p = P(fine);
+        ptg_mg_cfg o;
+        if (opt) o = *opt;
+        else ptg_mg_cfg_default(&o);
+        auto h = new ptg_hier;
+        try {
+            h->h = ptg::hier_build(p, metric, depth, o);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        h->fine = fine;
+        *out = h;
+    });
+}
+
+int ptg_hier_destroy(ptg_hier* h) {
+    return guard([&] {
+        if (!h) return;
+        for (auto& v : h->views) v.p.release();   // non-owning
+        delete h;
+    });
+}
+
+int ptg_hier_level(ptg_hier* h, int level, ptg_plan** plan_out) {
+    return guard([&] {
+        if (!h || level < 0 || level >= h->h->depth()) ptg::raise(PTG_ERR_CONFIG, "bad hierarchy level");
+        if (level == 0) {
+            *plan_out = h->fine;
+            return;
+        }
+        if (h->views.empty()) {
+            h->views.resize(h->h->depth());
+        }
+        ptg_plan& v = h->views[level];
+        if (!v.p) v.p.reset(h->h->levels[level]);
+        *plan_out = &v;
+    });
+}
+
+
+int ptg_mgopt_driver(ptg_hier* hh, const double* z0, const ptg_driver_cfg* cfg, double* z_out,
+                     ptg_report* rep, ptg_hist* hist, int hist_cap) {
+    return guard([&] {
+        if (!hh) ptg::raise(PTG_ERR_CONFIG, "null hierarchy");
+        ptg::Hier& h = *hh->h;
+        ptg::Plan& p = P(hh->fine);
+        sync_streams(h);
+        ptg_driver_cfg c;
+        if (cfg) c = *cfg;
+        else ptg_driver_cfg_default(&c);
+        const size_t len = p.nn();
+        ptg::DVec zd(p, len), zo(p, len);
+        ptg::plan_upload_c128(p, z0, zd.p);
+        ptg::Counter ctr;
+        std::vector<ptg_hist> hv;
+        ptg::SolveOut o = ptg::d_mgopt_driver(h, zd.p, c, ctr, zo.p, &hv);
+        if (z_out) ptg::plan_download_c128(p, zo.p, z_out);
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+        fill_report(rep, ctr, o.value, o.reason, copy_hist(hv, hist, hist_cap));
+    });
+}
+
+int ptg_mgopt_cycle_device(ptg_hier* hh, void* z, double* value, void* grad, ptg_report* rep) {
+    return guard([&] {
+        if (!hh) ptg::raise(PTG_ERR_CONFIG, "null hierarchy");
+        ptg::Hier& h = *hh->h;
+        ptg::Plan& p = P(hh->fine);
+        sync_streams(h);
+        const size_t len = p.nn();
+        ptg::DVec zo(p, len), go(p, len);
+        ptg::Counter ctr;
+        const double v = ptg::d_mgopt_cycle(h, 0, z, nullptr, ctr, value, grad, zo.p, go.p);
+        ptg::dev_copy(p.prec, z, zo.p, len, p.stream);
+        ptg::dev_copy(p.prec, grad, go.p, len, p.stream);
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+        *value = v;
+        fill_report(rep, ctr, v, PTG_STOP_MAXITERS, 0);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// common.cuh — shared device/host helpers for libptg (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/ptg.h"
+
+namespace ptg {
+
+// Status-carrying exception used inside the library; the C-ABI layer
+// (capi.cu) converts it to an int status + ptg_last_error() string.
+struct Status : std::runtime_error {
+    int code;
+    Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void raise(int code, const std::string& msg) { throw Status(code, msg); }
+
+#define PTG_CUDA(call)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            ::ptg::raise(PTG_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define PTG_CHECK_LAUNCH() PTG_CUDA(cudaGetLastError())
+
+// Complex scalar vector types: T = float (complex64) or double (complex128).
+template <typename T> struct V2;
+template <> struct V2<float> { using type = float2; };
+template <> struct V2<double> { using type = double2; };
+template <typename T> using cplx = typename V2<T>::type;
+
+template <typename T>
+__host__ __device__ __forceinline__ cplx<T> mk(T re, T im) {
+    cplx<T> r;
+    r.x = re;
+    r.y = im;
+    return r;
+}
+template <typename C>
+__host__ __device__ __forceinline__ C cadd(C a, C b) { C r; r.x = a.x + b.x; r.y = a.y + b.y; return r; }
+template <typename C>
+__host__ __device__ __forceinline__ C csub(C a, C b) { C r; r.x = a.x - b.x; r.y = a.y - b.y; return r; }
+template <typename C>
+__host__ __device__ __forceinline__ C cmul(C a, C b) {
+    C r;
+    r.x = a.x * b.x - a.y * b.y;
+    r.y = a.x * b.y + a.y * b.x;
+    return r;
+}
+// conj(a) * b
+template <typename C>
+__host__ __device__ __forceinline__ C cmulc(C a, C b) {
+    C r;
+    r.x = a.x * b.x + a.y * b.y;
+    r.y = a.x * b.y - a.y * b.x;
+    return r;
+}
+template <typename C, typename S>
+__host__ __device__ __forceinline__ C cscale(C a, S s) { C r; r.x = a.x * s; r.y = a.y * s; return r; }
+
+inline int ilog2(int n) { int l = 0; while ((1 << l) < n) ++l; return l; }
+inline bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+}  // namespace ptg

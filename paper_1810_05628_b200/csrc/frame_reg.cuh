@@ -1,0 +1,304 @@
+// frame_reg.cuh — register-resident fused frame kernel for complex64, M in {16,32,64}.
+//
+// Same computation as frame_kernel<OP_DISTANCE/OP_INTENSITY> (frame_kernels.cuh;
+// reference: objectives.cpp:59-103) but organised around the B200 register file:
+//
+//   * each thread owns one whole line (column, then row) of the M x M frame:
+//     M complex values = 2M fp32 registers;
+//   * a line FFT is a fully unrolled two-level Cooley-Tukey (8 x M/8) in
+//     registers with compile-time twiddles (folded into FMUL/FFMA immediates):
+//     no shared-memory traffic and no bit reversal inside a 1-D transform;
+//   * the 2-D transform needs exactly two transposes through shared memory
+//     (after the forward column pass, before the inverse column pass), with a
+//     (M+2)-element row pitch so 64/128-bit accesses are bank-conflict free;
+//   * global traffic is coalesced: the object window and probe are read
+//     column-per-thread (lanes walk a row), the contribution is written the
+//     same way; the per-pattern amplitudes sqrt(d_j) (the dominant HBM stream)
+//     are fetched by TMA bulk copies (cp.async.bulk + mbarrier), one per row,
+//     into padded rows of the (then idle) transpose buffer while the row FFT
+//     runs, and read back with conflict-free 128-bit loads.
+//
+// Order: gather(col) -> FFT cols -> transpose -> FFT rows -> spectral op +
+// fp64 misfit -> IFFT rows -> transpose -> IFFT cols -> conj(P) epilogue.
+#pragma once
+
+#include "fft.cuh"
+#include "frame_kernels.cuh"
+#include <utility>
+
+namespace ptg {
+
+// ------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbarrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+// 1-D TMA bulk copy global -> shared, completion counted on an mbarrier
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                             unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// ------------------------------------------------------ register line FFT
+// Compile-time twiddles: Taylor series evaluated by the compiler (constexpr),
+// argument reduced to [-pi, pi]; exact to ~1e-16, rounded once to fp32.
+__host__ __device__ constexpr double ct_sin(double x) {
+    double term = x, sum = x;
+    for (int k = 1; k < 24; ++k) {
+        term *= -x * x / ((2.0 * k) * (2.0 * k + 1.0));
+        sum += term;
+    }
+    return sum;
+}
+__host__ __device__ constexpr double ct_cos(double x) {
+    double term = 1.0, sum = 1.0;
+    for (int k = 1; k < 24; ++k) {
+        term *= -x * x / ((2.0 * k - 1.0) * (2.0 * k));
+        sum += term;
+    }
+    return sum;
+}
+__host__ __device__ constexpr double ct_angle(int idx, int L) {   // 2 pi idx / L in [-pi, pi]
+    const double pi = 3.14159265358979323846264338327950288;
+    double th = 2.0 * pi * (double)(idx % L) / (double)L;
+    return th > pi ? th - 2.0 * pi : th;
+}
+
+template <int N, class F, int... Is>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, Is...>) {
+    (f(std::integral_constant<int, Is>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    static_for_impl<N>(f, std::make_integer_sequence<int, N>{});
+}
+
+// v * W_L^E (forward W = e^{-2 pi i / L}), E a template constant: the
+// twiddle becomes FMUL/FFMA immediates; quarter turns are free swaps.
+template <int L, bool INV, int E>
+__device__ __forceinline__ float2 twiddle_mul(float2 v) {
+    constexpr int e = E % L;
+    if constexpr (e == 0) {
+        return v;
+    } else if constexpr (4 * e == L) {
+        return mul_negi<INV>(v);
+    } else if constexpr (2 * e == L) {
+        return make_float2(-v.x, -v.y);
+    } else if constexpr (4 * e == 3 * L) {
+        return mul_negi<!INV>(v);
+    } else {
+        constexpr float c = (float)ct_cos(ct_angle(e, L));
+        constexpr float s = INV ? (float)ct_sin(ct_angle(e, L)) : -(float)ct_sin(ct_angle(e, L));
+        return make_float2(v.x * c - v.y * s, v.x * s + v.y * c);
+    }
+}
+
+// In-place DFT of L values held in registers (natural order in and out).
+// L = A * B with A = 8:  n = B n1 + n2,  k = k1 + A k2.
+template <int L, bool INV>
+__device__ __forceinline__ void reg_fft(float2* x) {
+    if constexpr (L == 1) {
+    } else if constexpr (L == 2) {
+        dft2<INV>(x[0], x[1]);
+    } else if constexpr (L == 4) {
+        dft4<INV>(x[0], x[1], x[2], x[3]);
+    } else if constexpr (L == 8) {
+        dft8<INV>(x);
+    } else if constexpr (L == 16) {
+        dft16<INV>(x);
+    } else {
+        constexpr int A = 8, B = L / 8;
+        float2 y[L];
+        static_for<B>([&](auto n2c) {
+            constexpr int n2 = decltype(n2c)::value;
+            float2 t[A];
+#pragma unroll
+            for (int n1 = 0; n1 < A; ++n1) t[n1] = x[B * n1 + n2];
+            dft8<INV>(t);
+            static_for<A>([&](auto k1c) {
+                constexpr int k1 = decltype(k1c)::value;
+                y[k1 * B + n2] = twiddle_mul<L, INV, n2 * k1>(t[k1]);
+            });
+        });
+#pragma unroll
+        for (int k1 = 0; k1 < A; ++k1) {
+            float2 t[B];
+#pragma unroll
+            for (int n2 = 0; n2 < B; ++n2) t[n2] = y[k1 * B + n2];
+            reg_fft<B, INV>(t);
+#pragma unroll
+            for (int k2 = 0; k2 < B; ++k2) x[k1 + A * k2] = t[k2];
+        }
+    }
+}
+
+// --------------------------------------------------------------- kernel
+template <int M>
+constexpr int reg_frames_per_cta() { return M == 64 ? 1 : M == 32 ? 4 : 8; }
+
+template <int M>
+__host__ __device__ constexpr size_t reg_smem_bytes() {
+    return sizeof(float2) * (size_t)reg_frames_per_cta<M>() * M * (M + 2);
+}
+
+template <int M, int OP>
+__global__ void __launch_bounds__(M * reg_frames_per_cta<M>(), M == 64 ? 6 : 3)
+    frame_reg_kernel(FrameArgs<float> a, int count) {
+    constexpr int FPC = reg_frames_per_cta<M>();
+    constexpr int S = M + 2;    // float2 pitch of the transpose buffer
+    constexpr int AS = M + 4;   // float pitch of the staged amplitude rows (16 B pad)
+    constexpr int WPF = (M + 31) / 32;   // warps per frame (M >= 32)
+    static_assert(M * AS * sizeof(float) <= M * S * sizeof(float2), "amp staging must fit");
+
+    extern __shared__ __align__(128) unsigned char smem_reg[];
+    __shared__ __align__(8) unsigned long long bar[FPC];
+    __shared__ double red[FPC * WPF];
+
+    const int f = threadIdx.x / M;
+    const int t = threadIdx.x % M;
+    const int jl = blockIdx.x * FPC + f;
+    const bool live = jl < count;
+    const int j = a.first + (live ? jl : 0);
+    float2* buf = reinterpret_cast<float2*>(smem_reg) + (size_t)f * M * S;
+    float* ampbuf = reinterpret_cast<float*>(buf);
+
+    if (t == 0) mbar_init(&bar[f], M);
+    fence_mbarrier_init();
+
+    const int2 p = a.pos[j];
+    const int n = a.n, w = a.w;
+    const float2* __restrict__ probe = a.probe;
+    float2 x[M];
+
+    // 1. gather column t of psi = P o S_j x (lanes walk a row: coalesced)
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+        float2 v = make_float2(0.f, 0.f);
+        if (live && r < w && t < w) {
+            v = a.z[(size_t)(p.x + r) * n + (p.y + t)];
+            if (probe) v = cmul(probe[r * M + t], v);
+        }
+        x[r] = v;
+    }
+    reg_fft<M, false>(x);   // column FFTs
+
+    // 2. transpose through shared memory
+#pragma unroll
+    for (int k = 0; k < M; ++k) buf[k * S + t] = x[k];
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < M; c += 2) {
+        const float4 v = *reinterpret_cast<const float4*>(&buf[t * S + c]);
+        x[c] = make_float2(v.x, v.y);
+        x[c + 1] = make_float2(v.z, v.w);
+    }
+    __syncthreads();   // transpose reads complete before TMA reuses the buffer
+
+    // 3. TMA: this frame's amplitude row t -> padded smem row (overlaps the row FFT)
+    if (live) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bar[f], M * sizeof(float));
+        tma_bulk_g2s(ampbuf + t * AS, a.amp + (size_t)j * M * M + (size_t)t * M, M * sizeof(float), &bar[f]);
+    }
+    reg_fft<M, false>(x);   // row FFTs: x[c] = Psi[t][c]
+
+    // 4. spectral operator + misfit
+    double acc = 0.0;
+    if (live) {
+        mbar_wait(&bar[f], 0);
+#pragma unroll
+        for (int c = 0; c < M; c += 4) {
+            const float4 A4 = *reinterpret_cast<const float4*>(ampbuf + t * AS + c);
+            const float Av[4] = {A4.x, A4.y, A4.z, A4.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 W = x[c + q];
+                const float A = Av[q];
+                if constexpr (OP == OP_INTENSITY) {
+                    const float r = (W.x * W.x + W.y * W.y) - A;
+                    acc += (double)r * (double)r;
+                    x[c + q] = make_float2(W.x * r, W.y * r);
+                } else {
+                    // |W| and 1/|W| from one MUFU.RSQ (no IEEE divide slow path)
+                    const float m2 = W.x * W.x + W.y * W.y;
+                    const float inv = rsqrtf(m2);
+                    const bool nz = m2 > 0.f;
+                    const float mag = nz ? m2 * inv : 0.f;
+                    const float dl = mag - A;
+                    acc += (double)dl * (double)dl;
+                    x[c + q] = nz ? cscale(W, 1.f - A * inv) : make_float2(-A, 0.f);
+                }
+            }
+        }
+    }
+    // per-frame misfit reduction (fixed tree)
+    if constexpr (M >= 32) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if ((t & 31) == 0) red[f * WPF + t / 32] = acc;
+    } else {
+#pragma unroll
+        for (int o = M / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (t == 0) red[f] = acc;
+    }
+    reg_fft<M, true>(x);    // row IFFTs (unnormalised)
+    __syncthreads();        // amplitude reads + reduction partials complete
+    if (t == 0 && live) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < WPF; ++i) s += red[f * WPF + i];
+        a.misfit[j] = (OP == OP_DISTANCE) ? s / (2.0 * (double)M * (double)M) : 0.5 * s;
+    }
+
+    // 5. transpose back
+#pragma unroll
+    for (int c = 0; c < M; c += 2)
+        *reinterpret_cast<float4*>(&buf[t * S + c]) = make_float4(x[c].x, x[c].y, x[c + 1].x, x[c + 1].y);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < M; ++r) x[r] = buf[r * S + t];
+    reg_fft<M, true>(x);    // column IFFTs
+
+    // 6. epilogue: contribution added to the gradient (see frame_kernels.cuh)
+    if (live && t < w) {
+        const float sc = (OP == OP_DISTANCE) ? 1.f / (float(M) * float(M)) : 2.f;
+        float2* out = a.stash + (size_t)j * w * w + t;
+#pragma unroll
+        for (int r = 0; r < M; ++r) {
+            if (r < w) {
+                float2 v = cscale(x[r], sc);
+                if (probe) v = cmulc(probe[r * M + t], v);
+                out[(size_t)r * w] = v;
+            }
+        }
+    }
+}
+
+}  // namespace ptg

@@ -1,0 +1,843 @@
+// plan.cu — device-resident problem + the objective/gradient pipeline.
+//
+// plan_eval restates evaluate/phiDistance/phiIntensityGaussian
+// (/root/reference/proj/src/objectives.cpp:52-118) as, per pattern chunk:
+//   1. frame_kernel<OP>   one CTA per scan position: gather, 2-D FFT, spectral
+//                         misfit (fp64 block reduction), inverse FFT, conj(P)
+//                         epilogue -> stash[j] (w x w)
+//   2. k_overlap_gather   one CTA per 32x32 object tile: sums the stashes of
+//                         the windows covering the tile in ascending scan
+//                         order (the reference's accumulation order,
+//                         objectives.cpp:59-72), subtracts the shift v and
+//                         reduces <v,z>_R per tile — deterministic, no atomics
+//   3. k_finalize         value = sum_j misfit_j - sum_t dot_t (fixed tree)
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "frame_kernels.cuh"
+#include "frame_reg.cuh"
+#include "plan.cuh"
+#include "transfer.cuh"
+
+namespace ptg {
+
+Plan::~Plan() {
+    for (auto& e : ev_pool) {
+        if (e.a) cudaEventDestroy(e.a);
+        if (e.b) cudaEventDestroy(e.b);
+    }
+}
+
+void Plan::ev_begin(int kind) {
+    if (!timing) return;
+    if (ev_used == ev_pool.size()) {
+        EvPair e;
+        PTG_CUDA(cudaEventCreate(&e.a));
+        PTG_CUDA(cudaEventCreate(&e.b));
+        ev_pool.push_back(e);
+    }
+    ev_pool[ev_used].kind = kind;
+    PTG_CUDA(cudaEventRecord(ev_pool[ev_used].a, stream));
+}
+
+void Plan::ev_end() {
+    if (!timing) return;
+    PTG_CUDA(cudaEventRecord(ev_pool[ev_used].b, stream));
+    ++ev_used;
+}
+
+void Plan::timing_collect(double* ms, int64_t* cnt) {
+    ms[0] = ms[1] = 0.0;
+    cnt[0] = cnt[1] = 0;
+    for (size_t i = 0; i < ev_used; ++i) {
+        PTG_CUDA(cudaEventSynchronize(ev_pool[i].b));
+        float t = 0.f;
+        PTG_CUDA(cudaEventElapsedTime(&t, ev_pool[i].a, ev_pool[i].b));
+        ms[ev_pool[i].kind] += t;
+        cnt[ev_pool[i].kind] += 1;
+    }
+    ev_used = 0;
+}
+
+size_t Plan::device_bytes() const {
+    size_t b = pos.bytes + probe.bytes + amp.bytes + inten.bytes + stash.bytes + misfit.bytes +
+               dotp.bytes + value.bytes + scratch.bytes + flag.bytes + frame.bytes + zbuf.bytes +
+               vbuf.bytes + gbuf.bytes + stage.bytes;
+    for (const auto& c : chunks) b += c->tile_ids.bytes + c->tile_ptr.bytes + c->tile_list.bytes;
+    return b;
+}
+
+namespace {
+
+// ------------------------------------------------------------ frame launch
+template <int M>
+constexpr int frame_threads() {
+    return M <= 8 ? 32 : M == 16 ? 64 : M == 32 ? 128 : M == 64 ? 256 : 512;
+}
+
+template <typename T, int M, int OP>
+void launch_frame_t(const FrameArgs<T>& a, int count, cudaStream_t s) {
+    constexpr int NT = frame_threads<M>();
+    const size_t smem = frame_smem_bytes<T, M>(NT);
+    auto kern = frame_kernel<T, M, NT, OP>;
+    static bool attr = false;
+    if (!attr) {
+        PTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    kern<<<count, NT, smem, s>>>(a);
+    PTG_CHECK_LAUNCH();
+}
+
+template <typename T, int OP>
+void launch_frame_m(int M, const FrameArgs<T>& a, int count, cudaStream_t s) {
+    switch (M) {
+        case 1: launch_frame_t<T, 1, OP>(a, count, s); break;
+        case 2: launch_frame_t<T, 2, OP>(a, count, s); break;
+        case 4: launch_frame_t<T, 4, OP>(a, count, s); break;
+        case 8: launch_frame_t<T, 8, OP>(a, count, s); break;
+        case 16: launch_frame_t<T, 16, OP>(a, count, s); break;
+        case 32: launch_frame_t<T, 32, OP>(a, count, s); break;
+        case 64: launch_frame_t<T, 64, OP>(a, count, s); break;
+        case 128:
+            if constexpr (sizeof(T) == 4) {
+                launch_frame_t<T, 128, OP>(a, count, s);
+                break;
+            }
+            [[fallthrough]];
+        default:
+            raise(PTG_ERR_CONFIG, "frame side M=" + std::to_string(M) +
+                                      " exceeds the single-CTA shared-memory path for this precision");
+    }
+}
+
+// register-resident complex64 path (frame_reg.cuh) for the objective kernels
+template <int M, int OP>
+void launch_reg_t(const FrameArgs<float>& a, int count, cudaStream_t s) {
+    constexpr int FPC = reg_frames_per_cta<M>();
+    constexpr size_t smem = reg_smem_bytes<M>();
+    auto kern = frame_reg_kernel<M, OP>;
+    static bool attr = false;
+    if (!attr) {
+        PTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    kern<<<(count + FPC - 1) / FPC, M * FPC, smem, s>>>(a, count);
+    PTG_CHECK_LAUNCH();
+}
+
+template <int OP>
+bool launch_reg(int M, const FrameArgs<float>& a, int count, cudaStream_t s) {
+    switch (M) {
+        case 16: launch_reg_t<16, OP>(a, count, s); return true;
+        case 32: launch_reg_t<32, OP>(a, count, s); return true;
+        case 64: launch_reg_t<64, OP>(a, count, s); return true;
+        default: return false;
+    }
+}
+
+// objective frame kernel: register path for complex64 M in {16,32,64}, smem path otherwise
+template <typename T, int OP>
+void launch_objective(int M, const FrameArgs<T>& a, int count, cudaStream_t s) {
+    if constexpr (sizeof(T) == 4) {
+        if (launch_reg<OP>(M, a, count, s)) return;
+    }
+    launch_frame_m<T, OP>(M, a, count, s);
+}
+
+bool frame_supported(int prec, int M) {
+    return is_pow2(M) && (M <= 64 || (M == 128 && prec == PTG_C64));
+}
+
+template <typename T>
+FrameArgs<T> frame_args(Plan& p, const void* z, const T* amp) {
+    FrameArgs<T> a{};
+    a.z = static_cast<const cplx<T>*>(z);
+    a.probe = p.has_probe ? p.probe.as<const cplx<T>>() : nullptr;
+    a.pos = p.pos.as<const int2>();
+    a.amp = amp;
+    a.stash = p.stash.as<cplx<T>>();
+    a.misfit = p.misfit.as<double>();
+    a.n = p.n;
+    a.w = p.w;
+    return a;
+}
+
+// --------------------------------------------------------- overlap gather
+template <typename T>
+__global__ void __launch_bounds__(256) k_overlap_gather(
+    const cplx<T>* __restrict__ stash, int stash_first, const int2* __restrict__ pos,
+    const int* __restrict__ tile_ids, const int* __restrict__ tile_ptr,
+    const int* __restrict__ tile_list, int n, int w, int tiles_x, const cplx<T>* __restrict__ v,
+    const cplx<T>* __restrict__ z, cplx<T>* __restrict__ grad, double* __restrict__ dotp,
+    int accumulate) {
+    __shared__ double red[8];
+    const int t = tile_ids ? tile_ids[blockIdx.x] : blockIdx.x;
+    const int ty = t / tiles_x, tx = t % tiles_x;
+    const int x = tx * kTileW + threadIdx.x;
+    const int y = ty * kTileH + threadIdx.y;
+    // one pixel per thread; candidate windows fetched U at a time so their
+    // (independent) loads overlap, then added strictly in list (= scan) order
+    constexpr int U = 8;
+    cplx<T> acc = mk<T>(T(0), T(0));
+    const int e0 = tile_ptr[blockIdx.x], e1 = tile_ptr[blockIdx.x + 1];
+    for (int e = e0; e < e1; e += U) {
+        cplx<T> val[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            val[u] = mk<T>(T(0), T(0));
+            if (e + u < e1) {
+                const int j = __ldg(tile_list + e + u);
+                const int2 p = __ldg(pos + j);
+                const int cx = x - p.y, cy = y - p.x;
+                if ((unsigned)cx < (unsigned)w && (unsigned)cy < (unsigned)w)
+                    val[u] = stash[(size_t)(j - stash_first) * w * w + (size_t)cy * w + cx];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (e + u < e1) acc = cadd(acc, val[u]);
+    }
+    double d = 0.0;
+    if (x < n && y < n) {
+        const size_t idx = (size_t)y * n + x;
+        cplx<T> g = acc;
+        if (accumulate) g = cadd(grad[idx], g);
+        if (v) {
+            const cplx<T> vv = v[idx], zz = z[idx];
+            g = csub(g, vv);
+            d = (double)vv.x * (double)zz.x + (double)vv.y * (double)zz.y;
+        }
+        grad[idx] = g;
+    }
+    if (v) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        const int lin = threadIdx.y * 32 + threadIdx.x;
+        if ((lin & 31) == 0) red[lin >> 5] = d;
+        __syncthreads();
+        if (lin == 0) {
+            double s = 0.0;
+            for (int i = 0; i < 8; ++i) s += red[i];
+            dotp[blockIdx.x] = s;
+        }
+    }
+}
+
+// grad -= v ; dot partial per block (multi-chunk plans)
+template <typename T>
+__global__ void __launch_bounds__(256) k_shift(const cplx<T>* __restrict__ v, const cplx<T>* __restrict__ z,
+                                               cplx<T>* __restrict__ grad, size_t len, double* dotp) {
+    __shared__ double red[8];
+    const size_t chunk = (len + gridDim.x - 1) / gridDim.x;
+    const size_t lo = blockIdx.x * chunk, hi = min(lo + chunk, len);
+    double d = 0.0;
+    for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const cplx<T> vv = v[i], zz = z[i];
+        grad[i] = csub(grad[i], vv);
+        d += (double)vv.x * (double)zz.x + (double)vv.y * (double)zz.y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = d;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < 8; ++i) s += red[i];
+        dotp[blockIdx.x] = s;
+    }
+}
+
+// value = sum_j misfit_j - sum_t dotp_t, fixed partition + fixed tree
+__global__ void __launch_bounds__(256) k_finalize(const double* __restrict__ misfit, int N,
+                                                  const double* __restrict__ dotp, int ndot,
+                                                  double* __restrict__ out) {
+    __shared__ double red[8];
+    double m = 0.0, d = 0.0;
+    const int cm = (N + 255) / 256, cd = (ndot + 255) / 256;
+    for (int i = threadIdx.x * cm, e = min(i + cm, N); i < e; ++i) m += misfit[i];
+    for (int i = threadIdx.x * cd, e = min(i + cd, ndot); i < e; ++i) d += dotp[i];
+    double both[2] = {m, d};
+    double res[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        double x = both[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+        __syncthreads();
+        double s = 0.0;
+        if (threadIdx.x == 0)
+            for (int i = 0; i < 8; ++i) s += red[i];
+        res[q] = s;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = res[0] - res[1];
+}
+
+// --------------------------------------------------------------- data prep
+// d >= 0 check (checkPattern, objectives.cpp:12-18) + amp = sqrt(d)
+template <typename R>
+__global__ void k_prepare(const R* __restrict__ d, size_t len, R* __restrict__ amp,
+                          unsigned long long* bad) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x) {
+        const R x = d[i];
+        if (x < R(0)) atomicMin(bad, (unsigned long long)i);
+        amp[i] = sqrt(x);
+    }
+}
+
+template <typename R>
+__global__ void k_square(const R* __restrict__ a, size_t len, R* __restrict__ d) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x)
+        d[i] = a[i] * a[i];
+}
+
+inline int grid_for(size_t len) {
+    size_t g = (len + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    return g < 1 ? 1 : (int)g;
+}
+
+// ------------------------------------------------------------------ PIE
+// Strictly sequential sweep (solvers.cpp:244-251): one CTA walks the scan in
+// order; each projection is a full smem 2-D FFT pair; z is updated in global
+// memory and re-read (L2, __ldcg) by the next overlapping position.
+template <typename T, int M, int NT>
+__global__ void __launch_bounds__(NT) k_pie_sweep(cplx<T>* z, const cplx<T>* __restrict__ probe,
+                                                  const int2* __restrict__ pos,
+                                                  const T* __restrict__ amp, int N, int n, int w,
+                                                  const cplx<T>* __restrict__ wgt, T damping) {
+    using C = cplx<T>;
+    constexpr int S = frame_stride(M);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* buf = reinterpret_cast<C*>(smem_raw);
+    C* tw = buf + M * S;
+    build_twiddles<T>(tw, M);
+    const T inv = T(1) / (T(M) * T(M));
+    for (int k = 0; k < N; ++k) {
+        const int2 p = pos[k];
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < M * M; idx += NT) {
+            const int r = idx / M, c = idx % M;
+            C v = mk<T>(T(0), T(0));
+            if (r < w && c < w) {
+                const C zz = __ldcg(z + (size_t)(p.x + r) * n + (p.y + c));
+                v = probe ? cmul(probe[idx], zz) : zz;
+            }
+            buf[r * S + c] = v;
+        }
+        __syncthreads();
+        fft2d_smem<T, M, NT, false>(buf, S, tw);
+        const T* A = amp + (size_t)k * M * M;
+        for (int idx = threadIdx.x; idx < M * M; idx += NT) {
+            const C W = buf[(idx / M) * S + idx % M];
+            const T a = A[idx];
+            const T mag = sqrt(W.x * W.x + W.y * W.y);
+            buf[(idx / M) * S + idx % M] = mag > T(0) ? cscale(W, a / mag) : mk<T>(a, T(0));
+        }
+        __syncthreads();
+        fft2d_smem<T, M, NT, true>(buf, S, tw);
+        for (int idx = threadIdx.x; idx < w * w; idx += NT) {
+            const int r = idx / w, c = idx % w;
+            C* zp = z + (size_t)(p.x + r) * n + (p.y + c);
+            const C zz = __ldcg(zp);
+            const C psi = probe ? cmul(probe[r * M + c], zz) : zz;
+            const C dl = csub(cscale(buf[r * S + c], inv), psi);
+            C upd;
+            if (wgt) upd = cmul(wgt[idx], dl);
+            else upd = cscale(dl, damping);
+            __stcg(zp, cadd(zz, upd));
+        }
+    }
+}
+
+template <int M>
+constexpr int pie_threads() {
+    return M <= 8 ? 32 : M == 16 ? 64 : M == 32 ? 128 : M == 64 ? 512 : 1024;
+}
+
+template <typename T, int M>
+void launch_pie_t(Plan& p, void* z, const void* wgt, double damping) {
+    constexpr int NT = pie_threads<M>();
+    const size_t smem = sizeof(cplx<T>) * ((size_t)M * frame_stride(M) + M);
+    auto kern = k_pie_sweep<T, M, NT>;
+    static bool attr = false;
+    if (!attr) {
+        PTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    kern<<<1, NT, smem, p.stream>>>(static_cast<cplx<T>*>(z),
+                                    p.has_probe ? p.probe.as<const cplx<T>>() : nullptr,
+                                    p.pos.as<const int2>(), p.amp.as<const T>(), p.N, p.n, p.w,
+                                    static_cast<const cplx<T>*>(wgt), (T)damping);
+    PTG_CHECK_LAUNCH();
+    ++p.launches;
+}
+
+template <typename T>
+void launch_pie(Plan& p, void* z, const void* wgt, double damping) {
+    switch (p.M) {
+        case 1: launch_pie_t<T, 1>(p, z, wgt, damping); break;
+        case 2: launch_pie_t<T, 2>(p, z, wgt, damping); break;
+        case 4: launch_pie_t<T, 4>(p, z, wgt, damping); break;
+        case 8: launch_pie_t<T, 8>(p, z, wgt, damping); break;
+        case 16: launch_pie_t<T, 16>(p, z, wgt, damping); break;
+        case 32: launch_pie_t<T, 32>(p, z, wgt, damping); break;
+        case 64: launch_pie_t<T, 64>(p, z, wgt, damping); break;
+        case 128:
+            if constexpr (sizeof(T) == 4) {
+                launch_pie_t<T, 128>(p, z, wgt, damping);
+                break;
+            }
+            [[fallthrough]];
+        default:
+            raise(PTG_ERR_CONFIG, "pie: frame side M=" + std::to_string(p.M) +
+                                      " exceeds the single-CTA shared-memory path for this precision");
+    }
+}
+
+// --------------------------------------------------------- chunks / tiles
+void build_chunks(Plan& p) {
+    p.tiles_x = (p.n + kTileW - 1) / kTileW;
+    p.tiles_y = (p.n + kTileH - 1) / kTileH;
+    const size_t per = (size_t)p.w * p.w * p.celem();
+    const size_t budget = (size_t)2 << 30;   // stash bytes per chunk
+    int cs = p.N > 0 ? (int)std::min<size_t>((size_t)p.N, std::max<size_t>(1, budget / per)) : 1;
+    p.chunk_size = cs;
+    p.chunks.clear();
+    const int ntiles = p.tiles_x * p.tiles_y;
+    const int nchunks = p.N > 0 ? (p.N + cs - 1) / cs : 1;
+    for (int ci = 0; ci < nchunks; ++ci) {
+        auto c = std::make_unique<Chunk>();
+        c->first = ci * cs;
+        c->count = std::min(cs, p.N - c->first);
+        if (c->count < 0) c->count = 0;
+        std::vector<std::vector<int>> lists(ntiles);
+        for (int j = c->first; j < c->first + c->count; ++j) {
+            const int r0 = p.pos_h[2 * j], c0 = p.pos_h[2 * j + 1];
+            const int ty0 = r0 / kTileH, ty1 = (r0 + p.w - 1) / kTileH;
+            const int tx0 = c0 / kTileW, tx1 = (c0 + p.w - 1) / kTileW;
+            for (int ty = ty0; ty <= ty1; ++ty)
+                for (int tx = tx0; tx <= tx1; ++tx) lists[ty * p.tiles_x + tx].push_back(j);
+        }
+        std::vector<int> ids, ptr{0}, list;
+        c->all_tiles = (nchunks == 1);
+        for (int t = 0; t < ntiles; ++t) {
+            if (!c->all_tiles && lists[t].empty()) continue;
+            ids.push_back(t);
+            list.insert(list.end(), lists[t].begin(), lists[t].end());
+            ptr.push_back((int)list.size());
+        }
+        c->ntiles = (int)ids.size();
+        if (!c->all_tiles) {
+            c->tile_ids.alloc(ids.size() * sizeof(int));
+            if (!ids.empty()) PTG_CUDA(cudaMemcpy(c->tile_ids.p, ids.data(), ids.size() * sizeof(int), cudaMemcpyHostToDevice));
+        }
+        c->tile_ptr.alloc(ptr.size() * sizeof(int));
+        PTG_CUDA(cudaMemcpy(c->tile_ptr.p, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
+        c->tile_list.alloc(std::max<size_t>(1, list.size()) * sizeof(int));
+        if (!list.empty()) PTG_CUDA(cudaMemcpy(c->tile_list.p, list.data(), list.size() * sizeof(int), cudaMemcpyHostToDevice));
+        p.chunks.push_back(std::move(c));
+    }
+    p.stash.alloc(std::max<size_t>(1, (size_t)cs * p.w * p.w) * p.celem());
+    p.misfit.alloc(std::max<size_t>(1, (size_t)p.N) * sizeof(double));
+    // dot partials: one per tile (single chunk) or one per k_shift block
+    p.dotp.alloc(std::max<size_t>((size_t)ntiles, 1024) * sizeof(double));
+}
+
+void check_device(int device) {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        raise(PTG_ERR_CUDA, std::string("no CUDA device available (libptg has no CPU fallback): ") +
+                                cudaGetErrorString(e));
+    if (device < 0 || device >= count) raise(PTG_ERR_CUDA, "device ordinal out of range");
+    cudaDeviceProp prop;
+    PTG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        raise(PTG_ERR_CUDA, "libptg is built for sm_100a (B200); device " + std::to_string(device) +
+                                " is sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
+    PTG_CUDA(cudaSetDevice(device));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ create
+std::unique_ptr<Plan> plan_create(const ptg_plan_desc& d) {
+    if (d.n < 1) raise(PTG_ERR_GEOMETRY, "object side must be positive");
+    if (!is_pow2(d.M))
+        raise(PTG_ERR_GEOMETRY, "fft2: grid side must be a positive power of two, got " + std::to_string(d.M));
+    if (d.w < 1 || d.w > d.M || d.w > d.n)
+        raise(PTG_ERR_GEOMETRY, "window side " + std::to_string(d.w) + " must satisfy 1 <= w <= min(M, n)");
+    if (d.N < 0) raise(PTG_ERR_DOMAIN, "negative pattern count");
+    if (d.precision != PTG_C64 && d.precision != PTG_C128) raise(PTG_ERR_CONFIG, "unknown precision");
+    if (d.N > 0 && !d.positions) raise(PTG_ERR_CONFIG, "positions pointer is NULL");
+    for (int k = 0; k < d.N; ++k) {
+        const int r = d.positions[2 * k], c = d.positions[2 * k + 1];
+        if (r < 0 || c < 0 || r + d.w > d.n || c + d.w > d.n)
+            raise(PTG_ERR_GEOMETRY, "probe window [" + std::to_string(r) + "," + std::to_string(c) +
+                                        ")+" + std::to_string(d.w) + " does not fit an n=" +
+                                        std::to_string(d.n) + " grid");
+    }
+    if (!frame_supported(d.precision, d.M))
+        raise(PTG_ERR_CONFIG, "frame side M=" + std::to_string(d.M) + " is not supported for this precision yet");
+    check_device(d.device);
+
+    auto p = std::make_unique<Plan>();
+    p->n = d.n;
+    p->M = d.M;
+    p->w = d.w;
+    p->N = d.N;
+    p->prec = d.precision;
+    p->device = d.device;
+    p->has_probe = d.probe != nullptr;
+    p->pos_h.assign(d.positions, d.positions + 2 * (size_t)d.N);
+    PTG_CUDA(cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking));
+    p->stream = p->own_stream;
+    LaunchScope ls(*p);
+
+    p->pos.alloc(std::max<size_t>(1, (size_t)d.N) * sizeof(int2));
+    if (d.N) PTG_CUDA(cudaMemcpy(p->pos.p, d.positions, (size_t)d.N * sizeof(int2), cudaMemcpyHostToDevice));
+    if (p->has_probe) {
+        p->probe_h.assign(d.probe, d.probe + 2 * p->MM());
+        p->probe.alloc(p->MM() * p->celem());
+        p->stage.ensure(p->MM() * 16);
+        PTG_CUDA(cudaMemcpy(p->stage.p, d.probe, p->MM() * 16, cudaMemcpyHostToDevice));
+        dev_from_c128(p->prec, p->probe.p, p->stage.as<double>(), p->MM(), p->stream);
+    }
+    build_chunks(*p);
+    p->value.alloc(4 * sizeof(double));
+    p->scratch.alloc((kReduceBlocks + 2) * sizeof(double));
+    PTG_CUDA(cudaMemset(p->scratch.p, 0, p->scratch.bytes));
+    p->flag.alloc(sizeof(unsigned long long));
+    p->hval.ensure(4 * sizeof(double));
+    if (d.data) plan_set_data_host(*p, d.data, d.data_dtype);
+    PTG_CUDA(cudaStreamSynchronize(p->stream));
+    return p;
+}
+
+// ------------------------------------------------------------------- data
+static void validate_and_amp(Plan& p) {
+    const size_t len = (size_t)p.N * p.MM();
+    p.amp.ensure(std::max<size_t>(1, len) * p.relem());
+    unsigned long long init = ~0ull;
+    PTG_CUDA(cudaMemcpyAsync(p.flag.p, &init, sizeof init, cudaMemcpyHostToDevice, p.stream));
+    if (len) {
+        if (p.prec == PTG_C64)
+            k_prepare<float><<<grid_for(len), 256, 0, p.stream>>>(p.inten.as<const float>(), len, p.amp.as<float>(), p.flag.as<unsigned long long>());
+        else
+            k_prepare<double><<<grid_for(len), 256, 0, p.stream>>>(p.inten.as<const double>(), len, p.amp.as<double>(), p.flag.as<unsigned long long>());
+        PTG_CHECK_LAUNCH();
+        ++p.launches;
+    }
+    unsigned long long bad = 0;
+    PTG_CUDA(cudaMemcpyAsync(&bad, p.flag.p, sizeof bad, cudaMemcpyDeviceToHost, p.stream));
+    PTG_CUDA(cudaStreamSynchronize(p.stream));
+    if (bad != ~0ull) {
+        p.amp_valid = p.inten_valid = false;
+        raise(PTG_ERR_DOMAIN, "diffraction pattern has a negative intensity at index " +
+                                  std::to_string(bad % p.MM()));
+    }
+    p.amp_valid = true;
+    p.inten_valid = true;
+}
+
+void plan_set_data_device(Plan& p, const void* data, int dtype) {
+    LaunchScope ls(p);
+    const size_t len = (size_t)p.N * p.MM();
+    p.inten.ensure(std::max<size_t>(1, len) * p.relem());
+    if (len) dev_real_convert(p.prec, p.inten.p, dtype, data, len, p.stream);
+    validate_and_amp(p);
+}
+
+void plan_set_data_host(Plan& p, const void* data, int dtype) {
+    const size_t len = (size_t)p.N * p.MM();
+    if (!len) {
+        p.amp_valid = p.inten_valid = true;
+        return;
+    }
+    const size_t sb = len * (dtype == PTG_F32 ? 4 : 8);
+    DevMem tmp;
+    tmp.alloc(sb);
+    PTG_CUDA(cudaMemcpyAsync(tmp.p, data, sb, cudaMemcpyHostToDevice, p.stream));
+    plan_set_data_device(p, tmp.p, dtype);
+    PTG_CUDA(cudaStreamSynchronize(p.stream));
+}
+
+void plan_ensure(Plan& p, int metric) {
+    const size_t len = (size_t)p.N * p.MM();
+    if (metric == PTG_INTENSITY && !p.inten_valid) {
+        if (!p.amp_valid) raise(PTG_ERR_CONFIG, "plan has no diffraction data");
+        p.inten.ensure(std::max<size_t>(1, len) * p.relem());
+        if (len) {
+            if (p.prec == PTG_C64) k_square<float><<<grid_for(len), 256, 0, p.stream>>>(p.amp.as<const float>(), len, p.inten.as<float>());
+            else k_square<double><<<grid_for(len), 256, 0, p.stream>>>(p.amp.as<const double>(), len, p.inten.as<double>());
+            PTG_CHECK_LAUNCH();
+            ++p.launches;
+        }
+        p.inten_valid = true;
+    }
+    if (metric == PTG_DISTANCE && !p.amp_valid) {
+        if (!p.inten_valid) raise(PTG_ERR_CONFIG, "plan has no diffraction data");
+        validate_and_amp(p);
+    }
+    if (metric != PTG_DISTANCE && metric != PTG_INTENSITY) raise(PTG_ERR_CONFIG, "unknown metric kind");
+}
+
+// ------------------------------------------------------------------- eval
+template <typename T>
+static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad, double* value_dev) {
+    using C = cplx<T>;
+    const T* data = metric == PTG_DISTANCE ? p.amp.as<const T>() : p.inten.as<const T>();
+    const bool single = p.chunks.size() == 1;
+    if (!single) dev_fill_zero(p.prec, grad, p.nn(), p.stream);
+    int ndot = 0;
+    for (auto& cp : p.chunks) {
+        Chunk& c = *cp;
+        if (c.count > 0) {
+            FrameArgs<T> a = frame_args<T>(p, z, data);
+            a.first = c.first;
+            // frame_kernel writes stash[j*w*w]; offset the base so j - first maps to 0
+            a.stash = reinterpret_cast<C*>(p.stash.as<C>()) - (size_t)c.first * p.w * p.w;
+            p.ev_begin(0);
+            if (metric == PTG_DISTANCE) launch_objective<T, OP_DISTANCE>(p.M, a, c.count, p.stream);
+            else launch_objective<T, OP_INTENSITY>(p.M, a, c.count, p.stream);
+            p.ev_end();
+            ++p.launches;
+        }
+        if (c.ntiles > 0) {
+            dim3 blk(32, 8);
+            p.ev_begin(1);
+            k_overlap_gather<T><<<c.ntiles, blk, 0, p.stream>>>(
+                p.stash.as<const C>(), c.first, p.pos.as<const int2>(),
+                c.all_tiles ? nullptr : c.tile_ids.as<const int>(), c.tile_ptr.as<const int>(),
+                c.tile_list.as<const int>(), p.n, p.w, p.tiles_x,
+                single ? static_cast<const C*>(v) : nullptr, static_cast<const C*>(z),
+                static_cast<C*>(grad), p.dotp.as<double>(), single ? 0 : 1);
+            PTG_CHECK_LAUNCH();
+            p.ev_end();
+            ++p.launches;
+            if (single && v) ndot = c.ntiles;
+        }
+    }
+    if (!single && v) {
+        const int blocks = 1024;
+        k_shift<T><<<blocks, 256, 0, p.stream>>>(static_cast<const C*>(v), static_cast<const C*>(z),
+                                                 static_cast<C*>(grad), p.nn(), p.dotp.as<double>());
+        PTG_CHECK_LAUNCH();
+        ++p.launches;
+        ndot = blocks;
+    }
+    k_finalize<<<1, 256, 0, p.stream>>>(p.misfit.as<const double>(), p.N, p.dotp.as<const double>(), ndot,
+                                        value_dev);
+    PTG_CHECK_LAUNCH();
+    ++p.launches;
+}
+
+void plan_eval(Plan& p, int metric, const void* z, const void* v, void* grad, double* value_dev) {
+    LaunchScope ls(p);
+    plan_ensure(p, metric);
+    if (!grad) {
+        p.gbuf.ensure(p.nn() * p.celem());
+        grad = p.gbuf.p;
+    }
+    if (!value_dev) value_dev = p.value.as<double>();
+    if (p.prec == PTG_C64) eval_t<float>(p, metric, z, v, grad, value_dev);
+    else eval_t<double>(p, metric, z, v, grad, value_dev);
+}
+
+// --------------------------------------------------------------- simulate
+template <typename T>
+static void simulate_t(Plan& p, const void* z) {
+    FrameArgs<T> a = frame_args<T>(p, z, nullptr);
+    a.data_out = p.inten.as<T>();
+    for (auto& c : p.chunks) {
+        if (c->count <= 0) continue;
+        a.first = c->first;
+        launch_frame_m<T, OP_SIMULATE>(p.M, a, c->count, p.stream);
+        ++p.launches;
+    }
+}
+
+void plan_simulate(Plan& p, const void* z) {
+    LaunchScope ls(p);
+    const size_t len = (size_t)p.N * p.MM();
+    p.inten.ensure(std::max<size_t>(1, len) * p.relem());
+    if (p.prec == PTG_C64) simulate_t<float>(p, z);
+    else simulate_t<double>(p, z);
+    p.inten_valid = true;
+    p.amp_valid = false;
+    validate_and_amp(p);
+}
+
+// ---------------------------------------------------------------- project
+template <typename T>
+__global__ void k_roll(const cplx<T>* __restrict__ in, int M, int r0, int c0, cplx<T>* __restrict__ out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < M * M; i += gridDim.x * blockDim.x) {
+        const int r = i / M, c = i % M;
+        out[(size_t)((r + r0) % M) * M + (c + c0) % M] = in[i];
+    }
+}
+
+template <typename T>
+static void project_t(Plan& p, const void* z, int k, void* out) {
+    FrameArgs<T> a = frame_args<T>(p, z, p.amp.as<const T>());
+    p.frame.ensure(p.MM() * p.celem() * 2);
+    a.first = k;
+    a.frame_out = p.frame.as<cplx<T>>() - (size_t)k * p.MM();
+    launch_frame_m<T, OP_PROJECT>(p.M, a, 1, p.stream);
+    ++p.launches;
+    // ref mode: return the projection in object coordinates (objectives.cpp:42-50)
+    const int r0 = p.ref_mode() ? p.pos_h[2 * k] : 0, c0 = p.ref_mode() ? p.pos_h[2 * k + 1] : 0;
+    k_roll<T><<<grid_for(p.MM()), 256, 0, p.stream>>>(p.frame.as<const cplx<T>>(), p.M, r0, c0,
+                                                       static_cast<cplx<T>*>(out));
+    PTG_CHECK_LAUNCH();
+    ++p.launches;
+}
+
+void plan_project(Plan& p, const void* z, int k, void* out) {
+    LaunchScope ls(p);
+    if (k < 0 || k >= p.N) raise(PTG_ERR_DOMAIN, "pattern index out of range");
+    plan_ensure(p, PTG_DISTANCE);
+    if (p.prec == PTG_C64) project_t<float>(p, z, k, out);
+    else project_t<double>(p, z, k, out);
+}
+
+// -------------------------------------------------------------------- PIE
+void plan_pie_sweep(Plan& p, void* z, double gamma) {
+    LaunchScope ls(p);
+    if (gamma < 0.0) raise(PTG_ERR_CONFIG, "pie: gamma must be non-negative");
+    plan_ensure(p, PTG_DISTANCE);
+    if (p.N == 0) return;
+    const void* wgt = nullptr;
+    if (p.has_probe) {
+        // Alg. 1 weight: (|P|/max|P|) conj(P) / (|P|^2 + gamma), on the window
+        const int w = p.w, M = p.M;
+        double pmax = 0.0;
+        for (size_t i = 0; i < p.MM(); ++i) pmax = std::max(pmax, std::hypot(p.probe_h[2 * i], p.probe_h[2 * i + 1]));
+        std::vector<double> wg(2 * (size_t)w * w);
+        for (int r = 0; r < w; ++r)
+            for (int c = 0; c < w; ++c) {
+                const double* P = &p.probe_h[2 * ((size_t)r * M + c)];
+                const double a = std::hypot(P[0], P[1]);
+                const double s = (pmax > 0.0 ? a / pmax : 0.0) / (a * a + gamma);
+                wg[2 * ((size_t)r * w + c)] = s * P[0];
+                wg[2 * ((size_t)r * w + c) + 1] = -s * P[1];
+            }
+        p.stage.ensure(wg.size() * sizeof(double));
+        p.frame.ensure(p.MM() * p.celem() * 2 + (size_t)w * w * p.celem());
+        void* dw = static_cast<char*>(p.frame.p) + p.MM() * p.celem() * 2;
+        PTG_CUDA(cudaMemcpyAsync(p.stage.p, wg.data(), wg.size() * sizeof(double), cudaMemcpyHostToDevice, p.stream));
+        dev_from_c128(p.prec, dw, p.stage.as<double>(), (size_t)w * w, p.stream);
+        wgt = dw;
+    }
+    const double damping = 1.0 / (1.0 + gamma);
+    if (p.prec == PTG_C64) launch_pie<float>(p, z, wgt, damping);
+    else launch_pie<double>(p, z, wgt, damping);
+}
+
+// ------------------------------------------------------------- coarsening
+// buildCoarseLevel (multigrid.cpp:79-93) restated for the patch model:
+// n/2, M/2, w/2, floor(pos/2), probe -> restrictField(probe), data ->
+// restrictData, all on device.
+std::unique_ptr<Plan> plan_coarsen(Plan& f) {
+    if (f.n < 16) raise(PTG_ERR_GEOMETRY, "buildCoarseLevel: refuse to coarsen below n = 8");
+    if (f.w < 2 || f.w % 2 != 0)
+        raise(PTG_ERR_GEOMETRY, "buildCoarseLevel: window size must be even and >= 2, got " + std::to_string(f.w));
+    if (f.M < 4 || f.M % 4 != 0) raise(PTG_ERR_GEOMETRY, "restrictData: grid side must be a multiple of 4");
+    LaunchScope ls(f);
+    std::vector<int32_t> pos(f.pos_h.size());
+    for (size_t i = 0; i < pos.size(); ++i) pos[i] = f.pos_h[i] / 2;
+    std::vector<double> probe;
+    if (f.has_probe) {
+        probe.resize(2 * (size_t)(f.M / 2) * (f.M / 2));
+        const int M = f.M, MH = M / 2;
+        for (int r = 0; r < MH; ++r)
+            for (int c = 0; c < MH; ++c)
+                for (int q = 0; q < 2; ++q) {
+                    const double a = f.probe_h[2 * ((size_t)(2 * r) * M + 2 * c) + q];
+                    const double b = f.probe_h[2 * ((size_t)(2 * r) * M + 2 * c + 1) + q];
+                    const double cc = f.probe_h[2 * ((size_t)(2 * r + 1) * M + 2 * c) + q];
+                    const double d = f.probe_h[2 * ((size_t)(2 * r + 1) * M + 2 * c + 1) + q];
+                    probe[2 * ((size_t)r * MH + c) + q] = ((a + b) + (cc + d)) * 0.25;
+                }
+    }
+    ptg_plan_desc d{};
+    d.n = f.n / 2;
+    d.M = f.M / 2;
+    d.w = f.w / 2;
+    d.N = f.N;
+    d.positions = pos.data();
+    d.probe = f.has_probe ? probe.data() : nullptr;
+    d.data = nullptr;
+    d.precision = f.prec;
+    d.device = f.device;
+    auto c = plan_create(d);
+    // restrictData on device: intensities x 1/16 (or amplitudes x 1/4)
+    const size_t len = (size_t)c->N * c->MM();
+    const int dt = f.prec == PTG_C64 ? PTG_F32 : PTG_F64;
+    if (f.inten_valid) {
+        c->inten.ensure(std::max<size_t>(1, len) * c->relem());
+        PTG_CUDA(cudaStreamSynchronize(f.stream));
+        if (len) dev_restrict_data(dt, f.inten.p, f.N, f.M, c->inten.p, 1.0 / 16.0, c->stream);
+        c->inten_valid = true;
+        validate_and_amp(*c);
+    } else if (f.amp_valid) {
+        c->amp.ensure(std::max<size_t>(1, len) * c->relem());
+        PTG_CUDA(cudaStreamSynchronize(f.stream));
+        if (len) dev_restrict_data(dt, f.amp.p, f.N, f.M, c->amp.p, 0.25, c->stream);
+        c->amp_valid = true;
+    } else {
+        raise(PTG_ERR_CONFIG, "coarsen: fine plan has no data");
+    }
+    PTG_CUDA(cudaStreamSynchronize(c->stream));
+    return c;
+}
+
+// ------------------------------------------------------------ host helpers
+void plan_upload_c128(Plan& p, const double* host, void* dev) {
+    if (p.prec == PTG_C128) {
+        PTG_CUDA(cudaMemcpyAsync(dev, host, p.nn() * 16, cudaMemcpyHostToDevice, p.stream));
+        return;
+    }
+    p.stage.ensure(p.nn() * 16);
+    PTG_CUDA(cudaMemcpyAsync(p.stage.p, host, p.nn() * 16, cudaMemcpyHostToDevice, p.stream));
+    LaunchScope ls(p);
+    dev_from_c128(p.prec, dev, p.stage.as<double>(), p.nn(), p.stream);
+}
+
+void plan_download_c128(Plan& p, const void* dev, double* host) {
+    if (p.prec == PTG_C128) {
+        PTG_CUDA(cudaMemcpyAsync(host, dev, p.nn() * 16, cudaMemcpyDeviceToHost, p.stream));
+        return;
+    }
+    p.stage.ensure(p.nn() * 16);
+    LaunchScope ls(p);
+    dev_to_c128(p.prec, p.stage.as<double>(), dev, p.nn(), p.stream);
+    PTG_CUDA(cudaMemcpyAsync(host, p.stage.p, p.nn() * 16, cudaMemcpyDeviceToHost, p.stream));
+}
+
+double plan_read_scalar(Plan& p, const double* dev) {
+    PTG_CUDA(cudaMemcpyAsync(p.hval.p, dev, sizeof(double), cudaMemcpyDeviceToHost, p.stream));
+    PTG_CUDA(cudaStreamSynchronize(p.stream));
+    return *p.hval.as<double>();
+}
+
+bool plan_nonfinite(Plan& p, const void* x, size_t len) {
+    LaunchScope ls(p);
+    dev_nonfinite(p.prec, x, len, p.flag.as<int>(), p.stream);
+    int f = 0;
+    PTG_CUDA(cudaMemcpyAsync(&f, p.flag.p, sizeof(int), cudaMemcpyDeviceToHost, p.stream));
+    PTG_CUDA(cudaStreamSynchronize(p.stream));
+    return f != 0;
+}
+
+double plan_dot(Plan& p, const void* a, const void* b, size_t len) {
+    LaunchScope ls(p);
+    dev_dot(p.prec, a, b, len, p.scratch.as<double>(), p.value.as<double>() + 1, p.stream);
+    return plan_read_scalar(p, p.value.as<double>() + 1);
+}
+
+}  // namespace ptg

@@ -1,0 +1,136 @@
+// plan.cuh — a ptychography problem level resident on one device.
+//
+// Owns everything the hot path reads (positions, probe, amplitudes sqrt(d),
+// optional raw intensities) and the scratch it writes (per-pattern stash,
+// misfit partials, tile lists of the deterministic overlap-add).  Replaces
+// the reference's ScanGeometry + DiffractionStack + Objective bundle
+// (field.hpp:75-85, forward.hpp:22-27, objectives.hpp:18-26).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "blas.cuh"
+#include "common.cuh"
+
+namespace ptg {
+
+struct DevMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevMem() = default;
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+    ~DevMem() { release(); }
+    void alloc(size_t b) {
+        release();
+        if (b) PTG_CUDA(cudaMalloc(&p, b));
+        bytes = b;
+    }
+    void ensure(size_t b) { if (bytes < b) alloc(b); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class X> X* as() const { return static_cast<X*>(p); }
+};
+
+struct HostPinned {
+    void* p = nullptr;
+    size_t bytes = 0;
+    HostPinned() = default;
+    HostPinned(const HostPinned&) = delete;
+    HostPinned& operator=(const HostPinned&) = delete;
+    ~HostPinned() { if (p) cudaFreeHost(p); }
+    void ensure(size_t b) {
+        if (bytes >= b) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        PTG_CUDA(cudaMallocHost(&p, b));
+        bytes = b;
+    }
+    template <class X> X* as() const { return static_cast<X*>(p); }
+};
+
+// Patterns are processed in chunks whose stash fits the budget; each chunk
+// carries the CSR lists of the object tiles its windows touch.
+struct Chunk {
+    int first = 0, count = 0;
+    int ntiles = 0;          // tiles this chunk's gather visits
+    bool all_tiles = false;  // single-chunk plans visit every tile (tile id = block id)
+    DevMem tile_ids, tile_ptr, tile_list;
+};
+
+constexpr int kTileW = 32;   // overlap-add gather tile: 32 x 8 pixels, one per thread
+constexpr int kTileH = 8;
+
+struct Plan {
+    int n = 0, M = 0, w = 0, N = 0, prec = PTG_C64, device = 0;
+    bool has_probe = false;
+    std::vector<int32_t> pos_h;      // N x 2
+    std::vector<double> probe_h;     // M x M complex128 (empty if binary)
+
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+
+    DevMem pos, probe;
+    DevMem amp, inten;               // sqrt(d) and d, real type of the precision
+    bool amp_valid = false, inten_valid = false;
+
+    DevMem stash, misfit, dotp, value, scratch, flag, frame;
+    DevMem zbuf, vbuf, gbuf, stage;  // host-API working buffers
+    HostPinned hval;
+
+    // opt-in event timing of the frame kernel / gather (ptg_plan_set_timing)
+    struct EvPair { cudaEvent_t a = nullptr, b = nullptr; int kind = 0; };
+    bool timing = false;
+    std::vector<EvPair> ev_pool;
+    size_t ev_used = 0;
+    void ev_begin(int kind);
+    void ev_end();
+    void timing_collect(double* ms, int64_t* cnt);   // ms[2], cnt[2]
+
+    int tiles_x = 0, tiles_y = 0;
+    int chunk_size = 0;
+    std::vector<std::unique_ptr<Chunk>> chunks;
+    int64_t launches = 0;
+
+    ~Plan();
+    size_t celem() const { return prec == PTG_C64 ? 8 : 16; }
+    size_t relem() const { return prec == PTG_C64 ? 4 : 8; }
+    size_t nn() const { return (size_t)n * n; }
+    size_t MM() const { return (size_t)M * M; }
+    bool ref_mode() const { return !has_probe && M == n; }
+    size_t device_bytes() const;
+};
+
+// RAII: route blas/transfer launch counting into a plan
+struct LaunchScope {
+    int64_t* prev;
+    explicit LaunchScope(Plan& p) : prev(g_launch_counter) { g_launch_counter = &p.launches; }
+    ~LaunchScope() { g_launch_counter = prev; }
+};
+
+std::unique_ptr<Plan> plan_create(const ptg_plan_desc& d);
+// coarse plan built on device from a fine one (patch-model coarsening)
+std::unique_ptr<Plan> plan_coarsen(Plan& fine);
+void plan_set_data_host(Plan& p, const void* data, int dtype);
+void plan_set_data_device(Plan& p, const void* data, int dtype);
+void plan_ensure(Plan& p, int metric);   // make amp / inten valid for metric
+
+// objective + gradient on device buffers (plan precision); grad may be null
+void plan_eval(Plan& p, int metric, const void* z, const void* v, void* grad, double* value_dev);
+void plan_simulate(Plan& p, const void* z);
+void plan_project(Plan& p, const void* z, int k, void* frame_out);
+// one PIE sweep in place on device object z
+void plan_pie_sweep(Plan& p, void* z, double gamma);
+
+// host helpers
+void plan_upload_c128(Plan& p, const double* host, void* dev);   // host c128 -> device prec
+void plan_download_c128(Plan& p, const void* dev, double* host);
+double plan_read_scalar(Plan& p, const double* dev);              // synchronising read
+bool plan_nonfinite(Plan& p, const void* x, size_t len);
+double plan_dot(Plan& p, const void* a, const void* b, size_t len);   // synchronising
+
+}  // namespace ptg

@@ -1,0 +1,110 @@
+// solvers.cuh — GPU-resident solver control flow (host C++ over device vectors).
+//
+// Restates /root/reference/proj/src/solvers.cpp:19-141 (two-loop LBFGS,
+// backtracking line search) and multigrid.cpp:95-227 (hierarchy, V-cycle,
+// driver) with every iterate, gradient, curvature pair and shift resident in
+// HBM.  Only scalars (objective values, dot products) cross PCIe, one
+// synchronising read each.  Accounting (EvalCounter: charge before evaluate,
+// weight 4^-level) and all control decisions are identical to the reference.
+#pragma once
+
+#include <deque>
+#include <memory>
+#include <vector>
+
+#include "plan.cuh"
+
+namespace ptg {
+
+struct Counter {
+    double weighted = 0.0;
+    long per_level[16] = {};
+    void record(int level, double w) {
+        weighted += w;
+        if (level >= 0 && level < 16) ++per_level[level];
+    }
+};
+
+// device vector in a plan's precision, stream-ordered allocation
+struct DVec {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaStream_t s = nullptr;
+    DVec() = default;
+    DVec(Plan& pl, size_t len) { alloc(pl, len); }
+    DVec(const DVec&) = delete;
+    DVec& operator=(const DVec&) = delete;
+    DVec(DVec&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s) { o.p = nullptr; o.bytes = 0; }
+    DVec& operator=(DVec&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            bytes = o.bytes;
+            s = o.s;
+            o.p = nullptr;
+            o.bytes = 0;
+        }
+        return *this;
+    }
+    ~DVec() { release(); }
+    void alloc(Plan& pl, size_t len) {
+        release();
+        s = pl.stream;
+        bytes = len * pl.celem();
+        if (bytes) PTG_CUDA(cudaMallocAsync(&p, bytes, s));
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+// CountedObjective (solvers.hpp:28-37) bound to a device plan
+struct DObj {
+    Plan* plan = nullptr;
+    int metric = PTG_DISTANCE;
+    const void* v = nullptr;   // shift (device), nullptr = none
+    int level = 0;
+    double weight = 1.0;
+    double eval(Counter& c, const void* z, void* grad) const;
+};
+
+struct SolveOut {
+    double value = 0.0;
+    int reason = PTG_STOP_MAXITERS;
+};
+
+// solvers.cpp:61-85; writes the accepted point into z_out/g_out
+struct LsOut {
+    double alpha = 0.0, value = 0.0;
+    bool stalled = false;
+    int trials = 0;
+};
+LsOut d_linesearch(const DObj& obj, const void* z, const void* dir, Counter& ctr, int max_trials,
+                   const double* phi0, void* z_out, void* g_out);
+
+// solvers.cpp:87-141.  warm_g (device) with *warm_value, or null to evaluate.
+SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Counter& ctr,
+                 const double* warm_value, const void* warm_g, void* z_out, void* g_out,
+                 std::vector<ptg_hist>* hist);
+
+struct Hier {
+    Plan* fine = nullptr;
+    std::vector<std::unique_ptr<Plan>> owned;   // levels 1..depth-1
+    std::vector<Plan*> levels;
+    int metric = PTG_DISTANCE;
+    ptg_mg_cfg opt{};
+    int coarsest_iters = 3;
+    int depth() const { return (int)levels.size(); }
+};
+
+std::unique_ptr<Hier> hier_build(Plan& fine, int metric, int depth, const ptg_mg_cfg& opt);
+// multigrid.cpp:117-169 ; v may be null (= zero shift)
+double d_mgopt_cycle(Hier& h, int level, const void* z, const void* v, Counter& ctr,
+                     const double* warm_value, const void* warm_g, void* z_out, void* g_out);
+// multigrid.cpp:171-227
+SolveOut d_mgopt_driver(Hier& h, const void* z0, const ptg_driver_cfg& cfg, Counter& ctr,
+                        void* z_out, std::vector<ptg_hist>* hist);
+
+}  // namespace ptg

@@ -1,0 +1,14 @@
+// transfer.cuh — MG/OPT grid-transfer operators (see transfer.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace ptg {
+
+void dev_restrict_field(int prec, const void* fine, int n, void* coarse, cudaStream_t s);
+void dev_prolong_field(int prec, const void* coarse, int nH, void* fine, cudaStream_t s);
+// scale = 1/16 for intensities (multigrid.cpp:74), 1/4 for amplitudes sqrt(d)
+void dev_restrict_data(int dtype, const void* fine, int N, int M, void* coarse, double scale,
+                       cudaStream_t s);
+
+}  // namespace ptg

@@ -1,0 +1,203 @@
+"""GPU parity: libptg (through the C-ABI) vs the CPU oracle / compiled reference.
+
+Tolerances (BASELINE.json north_star): complex64 objective 1e-5 relative and
+gradient 1e-4 relative L2; complex128 1e-10.  Integer/index work (transfers)
+is bit-exact.
+"""
+import numpy as np
+import pytest
+
+from conftest import rand_field, rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+C64_VAL, C64_GRAD = 1e-5, 1e-4
+C128_TOL = 1e-10
+
+
+def _round64(a):
+    return np.asarray(a).astype(np.complex64).astype(np.complex128)
+
+
+def _patch_case(oracle, cfg, precision, metric=0, with_shift=True, seed=5):
+    from paper_1810_05628_b200 import Plan, synth
+    obj, probe, pos = synth.make_inputs(cfg)
+    z = obj * 0.9 + 0.05 * rand_field(cfg.n, seed)   # an iterate near the truth
+    v = 0.01 * rand_field(cfg.n, seed + 1) if with_shift else None
+    data = oracle.simulate(cfg.n, cfg.M, cfg.w, pos, obj, probe)
+    if precision == "c64":
+        z, probe = _round64(z), _round64(probe)
+        v = _round64(v) if v is not None else None
+        data = data.astype(np.float32)
+    p = oracle.Problem(cfg.n, cfg.M, cfg.w, pos, data.astype(np.float64), probe, metric)
+    want_v, want_g = oracle.evaluate(p, z, v)
+    plan = Plan(cfg.n, cfg.M, cfg.w, pos, data, probe, precision=precision)
+    got_v, got_g = plan.evaluate(z, v, metric=metric)
+    return got_v, got_g, want_v, want_g, plan, (z, v)
+
+
+@pytest.mark.parametrize("cid", [1, 2])
+def test_config_eval_c64(oracle, cid):
+    from paper_1810_05628_b200 import synth
+    cfg = synth.CONFIGS[cid]
+    gv, gg, wv, wg, _, _ = _patch_case(oracle, cfg, "c64")
+    assert rel(gv, wv) <= C64_VAL, (gv, wv)
+    assert rel_l2(gg, wg) <= C64_GRAD
+
+
+def test_config1_eval_c128(oracle):
+    from paper_1810_05628_b200 import synth
+    gv, gg, wv, wg, _, _ = _patch_case(oracle, synth.CONFIGS[1], "c128")
+    assert rel(gv, wv) <= C128_TOL
+    assert rel_l2(gg, wg) <= C128_TOL
+
+
+@pytest.mark.parametrize("precision,tv,tg", [("c64", C64_VAL, C64_GRAD), ("c128", C128_TOL, C128_TOL)])
+@pytest.mark.parametrize("M", [1, 2, 4, 8, 16, 32, 64])
+def test_frame_sizes(oracle, precision, tv, tg, M):
+    from paper_1810_05628_b200 import synth
+    n = max(2 * M, 8)
+    steps = 3 if M > 1 else 2
+    step = max(1, M // 2) if M > 1 else 1
+    n = max(n, (steps - 1) * step + M)
+    cfg = synth.Config(0, n, M, steps, step, 2.0, max(M / 4, 1.0), 0.01, precision)
+    gv, gg, wv, wg, _, _ = _patch_case(oracle, cfg, precision)
+    assert rel(gv, wv, floor=1e-12) <= tv
+    assert rel_l2(gg, wg) <= tg
+
+
+def test_frame_128_c64(oracle):
+    from paper_1810_05628_b200 import synth
+    cfg = synth.Config(0, 256, 128, 3, 64, 6.0, 32.0, 0.0, "c64", jitter=2)
+    gv, gg, wv, wg, _, _ = _patch_case(oracle, cfg, "c64")
+    assert rel(gv, wv) <= C64_VAL
+    assert rel_l2(gg, wg) <= C64_GRAD
+
+
+@pytest.mark.parametrize("precision", ["c64", "c128"])
+def test_intensity_metric(oracle, precision):
+    from paper_1810_05628_b200 import synth
+    cfg = synth.small_config(precision=precision)
+    gv, gg, wv, wg, _, _ = _patch_case(oracle, cfg, precision, metric=1)
+    tol = C128_TOL if precision == "c128" else C64_GRAD
+    assert rel(gv, wv) <= tol
+    assert rel_l2(gg, wg) <= tol
+
+
+def test_ref_mode_against_reference(reference):
+    """Binary window, M == n: the reference library itself is the oracle."""
+    from paper_1810_05628_b200 import Plan
+    n, w, s = 32, 16, 8
+    win = reference.ref_raster(n, w, s)
+    pos = win[:, :2]
+    zt = rand_field(n, 11)
+    z = rand_field(n, 12)
+    v = rand_field(n, 13)
+    data = reference.ref_simulate(n, w, pos, zt)
+    plan = Plan(n, n, w, pos, data, None, precision="c128")
+    for metric in (0, 1):
+        wv, wg = reference.ref_evaluate(metric, n, w, pos, data, z, v)
+        gv, gg = plan.evaluate(z, v, metric=metric)
+        assert rel(gv, wv) <= C128_TOL
+        assert rel_l2(gg, wg) <= C128_TOL
+    # projectModulus returns object coordinates in ref mode
+    for k in (0, 4, 8):
+        want = reference.ref_project_modulus(n, win[k], data[k], z)
+        got = plan.project_modulus(z, k)
+        assert rel_l2(got, want) <= C128_TOL
+
+
+def test_simulate_matches_oracle(oracle):
+    from paper_1810_05628_b200 import Plan, synth
+    for precision, tol in (("c128", 1e-12), ("c64", 2e-6)):
+        cfg = synth.small_config(precision=precision)
+        obj, probe, pos = synth.make_inputs(cfg)
+        want = oracle.simulate(cfg.n, cfg.M, cfg.w, pos, obj, probe)
+        plan = Plan(cfg.n, cfg.M, cfg.w, pos, None, probe, precision=precision)
+        got = plan.simulate(obj)
+        assert rel_l2(got, want) <= tol
+
+
+def test_project_modulus_patch(oracle):
+    from paper_1810_05628_b200 import Plan, synth
+    cfg = synth.small_config(precision="c128")
+    obj, probe, pos = synth.make_inputs(cfg)
+    data = oracle.simulate(cfg.n, cfg.M, cfg.w, pos, obj, probe)
+    z = rand_field(cfg.n, 3)
+    p = oracle.Problem(cfg.n, cfg.M, cfg.w, pos, data, probe)
+    plan = Plan(cfg.n, cfg.M, cfg.w, pos, data, probe, precision="c128")
+    for k in (0, 10, cfg.N - 1):
+        assert rel_l2(plan.project_modulus(z, k), oracle.project_modulus(p, z, k)) <= C128_TOL
+
+
+def test_fixed_point_at_truth():
+    """test_objectives.cpp:207-217: Phi ~ 0 and grad ~ 0 at the true object."""
+    from paper_1810_05628_b200 import Plan, synth
+    cfg = synth.small_config(precision="c128")
+    obj, probe, pos = synth.make_inputs(cfg)
+    plan = Plan(cfg.n, cfg.M, cfg.w, pos, None, probe, precision="c128")
+    plan.simulate(obj, copy_out=False)
+    val, g = plan.evaluate(obj)
+    assert 0.0 <= val <= 1e-20
+    assert np.linalg.norm(g) <= 1e-9
+
+
+def test_determinism_bitwise(oracle):
+    from paper_1810_05628_b200 import synth
+    gv, gg, _, _, plan, (z, v) = _patch_case(oracle, synth.CONFIGS[2], "c64")
+    for _ in range(3):
+        v2, g2 = plan.evaluate(z, v)
+        assert v2 == gv
+        assert np.array_equal(g2, gg)
+
+
+def test_empty_scan(oracle):
+    from paper_1810_05628_b200 import Plan
+    n = 16
+    z, v = rand_field(n, 1), rand_field(n, 2)
+    plan = Plan(n, 8, 8, np.zeros((0, 2), np.int32), np.zeros((0, 8, 8)), None, precision="c128")
+    val, g = plan.evaluate(z, v)
+    assert val == pytest.approx(-np.sum(v.real * z.real + v.imag * z.imag), rel=1e-14)
+    assert np.array_equal(g, -v)
+
+
+def test_single_pixel_analytic():
+    """test_objectives.cpp:185-205: 1x1 analytic values."""
+    from paper_1810_05628_b200 import Plan
+    z = np.array([[1.0 + 0j]])
+    pos = np.zeros((1, 2), np.int32)
+    plan = Plan(1, 1, 1, pos, np.array([[[4.0]]]), None, precision="c128")
+    val, g = plan.evaluate(z)
+    assert val == pytest.approx(0.5, rel=1e-15)
+    assert g[0, 0].real == pytest.approx(-1.0, rel=1e-15)
+    plan0 = Plan(1, 1, 1, pos, np.array([[[0.0]]]), None, precision="c128")
+    val, g = plan0.evaluate(z, metric=1)
+    assert val == pytest.approx(0.5, rel=1e-15)
+    assert g[0, 0].real == pytest.approx(2.0, rel=1e-15)
+
+
+def test_validation_errors():
+    from paper_1810_05628_b200 import DomainError, GeometryError, Plan
+    pos = np.array([[0, 0]], np.int32)
+    d = np.ones((1, 8, 8))
+    d[0, 3, 3] = -1e-9
+    with pytest.raises(DomainError):
+        Plan(8, 8, 4, pos, d, None, precision="c128")
+    with pytest.raises(GeometryError):
+        Plan(8, 8, 4, np.array([[6, 0]], np.int32), np.ones((1, 8, 8)), None)
+    with pytest.raises(GeometryError):
+        Plan(12, 12, 4, pos, np.ones((1, 12, 12)), None)
+    plan = Plan(8, 8, 4, pos, np.ones((1, 8, 8)), None, precision="c128")
+    with pytest.raises(DomainError):
+        plan.set_data(d)
+
+
+def test_transfers_bitexact(oracle):
+    from paper_1810_05628_b200 import prolong_field, restrict_data, restrict_field
+    f = rand_field(64, 7)
+    assert np.array_equal(restrict_field(f), oracle.restrict_field(f))
+    c = rand_field(32, 8)
+    assert np.array_equal(prolong_field(c), oracle.prolong_field(c))
+    assert np.array_equal(restrict_field(prolong_field(c)), c)   # multigrid.hpp:11-13
+    d = np.abs(np.random.default_rng(9).normal(size=(5, 32, 32)))
+    assert np.array_equal(restrict_data(d), oracle.restrict_data(d))
