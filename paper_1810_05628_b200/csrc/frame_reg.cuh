@@ -1,4 +1,4 @@
-// frame_reg.cuh — register-resident fused frame kernel for complex64, M in {16,32,64}.
+// frame_reg.cuh — register-resident line FFT + TMA/mbarrier helpers (complex64).
 //
 // Same computation as frame_kernel<OP_DISTANCE/OP_INTENSITY> (frame_kernels.cuh;
 // reference: objectives.cpp:59-103) but organised around the B200 register file:
@@ -64,6 +64,14 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phas
         "}\n" ::"r"(smem_u32(bar)),
         "r"(phase)
         : "memory");
+}
+
+// read-only 64-bit load pinned in program order (volatile asm): bounds how
+// many loads the compiler hoists while a whole line is live in registers
+__device__ __forceinline__ float2 ldg_pinned(const float2* p) {
+    float2 v;
+    asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return v;
 }
 
 // ------------------------------------------------------ register line FFT
@@ -155,148 +163,6 @@ __device__ __forceinline__ void reg_fft(float2* x) {
             reg_fft<B, INV>(t);
 #pragma unroll
             for (int k2 = 0; k2 < B; ++k2) x[k1 + A * k2] = t[k2];
-        }
-    }
-}
-
-// --------------------------------------------------------------- kernel
-template <int M>
-constexpr int reg_frames_per_cta() { return M == 64 ? 1 : M == 32 ? 4 : 8; }
-
-template <int M>
-__host__ __device__ constexpr size_t reg_smem_bytes() {
-    return sizeof(float2) * (size_t)reg_frames_per_cta<M>() * M * (M + 2);
-}
-
-template <int M, int OP>
-__global__ void __launch_bounds__(M * reg_frames_per_cta<M>(), M == 64 ? 6 : 3)
-    frame_reg_kernel(FrameArgs<float> a, int count) {
-    constexpr int FPC = reg_frames_per_cta<M>();
-    constexpr int S = M + 2;    // float2 pitch of the transpose buffer
-    constexpr int AS = M + 4;   // float pitch of the staged amplitude rows (16 B pad)
-    constexpr int WPF = (M + 31) / 32;   // warps per frame (M >= 32)
-    static_assert(M * AS * sizeof(float) <= M * S * sizeof(float2), "amp staging must fit");
-
-    extern __shared__ __align__(128) unsigned char smem_reg[];
-    __shared__ __align__(8) unsigned long long bar[FPC];
-    __shared__ double red[FPC * WPF];
-
-    const int f = threadIdx.x / M;
-    const int t = threadIdx.x % M;
-    const int jl = blockIdx.x * FPC + f;
-    const bool live = jl < count;
-    const int j = a.first + (live ? jl : 0);
-    float2* buf = reinterpret_cast<float2*>(smem_reg) + (size_t)f * M * S;
-    float* ampbuf = reinterpret_cast<float*>(buf);
-
-    if (t == 0) mbar_init(&bar[f], M);
-    fence_mbarrier_init();
-
-    const int2 p = a.pos[j];
-    const int n = a.n, w = a.w;
-    const float2* __restrict__ probe = a.probe;
-    float2 x[M];
-
-    // 1. gather column t of psi = P o S_j x (lanes walk a row: coalesced)
-#pragma unroll
-    for (int r = 0; r < M; ++r) {
-        float2 v = make_float2(0.f, 0.f);
-        if (live && r < w && t < w) {
-            v = a.z[(size_t)(p.x + r) * n + (p.y + t)];
-            if (probe) v = cmul(probe[r * M + t], v);
-        }
-        x[r] = v;
-    }
-    reg_fft<M, false>(x);   // column FFTs
-
-    // 2. transpose through shared memory
-#pragma unroll
-    for (int k = 0; k < M; ++k) buf[k * S + t] = x[k];
-    __syncthreads();
-#pragma unroll
-    for (int c = 0; c < M; c += 2) {
-        const float4 v = *reinterpret_cast<const float4*>(&buf[t * S + c]);
-        x[c] = make_float2(v.x, v.y);
-        x[c + 1] = make_float2(v.z, v.w);
-    }
-    __syncthreads();   // transpose reads complete before TMA reuses the buffer
-
-    // 3. TMA: this frame's amplitude row t -> padded smem row (overlaps the row FFT)
-    if (live) {
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&bar[f], M * sizeof(float));
-        tma_bulk_g2s(ampbuf + t * AS, a.amp + (size_t)j * M * M + (size_t)t * M, M * sizeof(float), &bar[f]);
-    }
-    reg_fft<M, false>(x);   // row FFTs: x[c] = Psi[t][c]
-
-    // 4. spectral operator + misfit
-    double acc = 0.0;
-    if (live) {
-        mbar_wait(&bar[f], 0);
-#pragma unroll
-        for (int c = 0; c < M; c += 4) {
-            const float4 A4 = *reinterpret_cast<const float4*>(ampbuf + t * AS + c);
-            const float Av[4] = {A4.x, A4.y, A4.z, A4.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const float2 W = x[c + q];
-                const float A = Av[q];
-                if constexpr (OP == OP_INTENSITY) {
-                    const float r = (W.x * W.x + W.y * W.y) - A;
-                    acc += (double)r * (double)r;
-                    x[c + q] = make_float2(W.x * r, W.y * r);
-                } else {
-                    // |W| and 1/|W| from one MUFU.RSQ (no IEEE divide slow path)
-                    const float m2 = W.x * W.x + W.y * W.y;
-                    const float inv = rsqrtf(m2);
-                    const bool nz = m2 > 0.f;
-                    const float mag = nz ? m2 * inv : 0.f;
-                    const float dl = mag - A;
-                    acc += (double)dl * (double)dl;
-                    x[c + q] = nz ? cscale(W, 1.f - A * inv) : make_float2(-A, 0.f);
-                }
-            }
-        }
-    }
-    // per-frame misfit reduction (fixed tree)
-    if constexpr (M >= 32) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if ((t & 31) == 0) red[f * WPF + t / 32] = acc;
-    } else {
-#pragma unroll
-        for (int o = M / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (t == 0) red[f] = acc;
-    }
-    reg_fft<M, true>(x);    // row IFFTs (unnormalised)
-    __syncthreads();        // amplitude reads + reduction partials complete
-    if (t == 0 && live) {
-        double s = 0.0;
-#pragma unroll
-        for (int i = 0; i < WPF; ++i) s += red[f * WPF + i];
-        a.misfit[j] = (OP == OP_DISTANCE) ? s / (2.0 * (double)M * (double)M) : 0.5 * s;
-    }
-
-    // 5. transpose back
-#pragma unroll
-    for (int c = 0; c < M; c += 2)
-        *reinterpret_cast<float4*>(&buf[t * S + c]) = make_float4(x[c].x, x[c].y, x[c + 1].x, x[c + 1].y);
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < M; ++r) x[r] = buf[r * S + t];
-    reg_fft<M, true>(x);    // column IFFTs
-
-    // 6. epilogue: contribution added to the gradient (see frame_kernels.cuh)
-    if (live && t < w) {
-        const float sc = (OP == OP_DISTANCE) ? 1.f / (float(M) * float(M)) : 2.f;
-        float2* out = a.stash + (size_t)j * w * w + t;
-#pragma unroll
-        for (int r = 0; r < M; ++r) {
-            if (r < w) {
-                float2 v = cscale(x[r], sc);
-                if (probe) v = cmulc(probe[r * M + t], v);
-                out[(size_t)r * w] = v;
-            }
         }
     }
 }

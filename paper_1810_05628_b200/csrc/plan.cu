@@ -15,8 +15,10 @@
 #include <cmath>
 #include <cstring>
 
+#include <cudaTypedefs.h>
+
 #include "frame_kernels.cuh"
-#include "frame_reg.cuh"
+#include "frame_tma.cuh"
 #include "plan.cuh"
 #include "transfer.cuh"
 
@@ -112,38 +114,105 @@ void launch_frame_m(int M, const FrameArgs<T>& a, int count, cudaStream_t s) {
     }
 }
 
-// register-resident complex64 path (frame_reg.cuh) for the objective kernels
-template <int M, int OP>
-void launch_reg_t(const FrameArgs<float>& a, int count, cudaStream_t s) {
-    constexpr int FPC = reg_frames_per_cta<M>();
-    constexpr size_t smem = reg_smem_bytes<M>();
-    auto kern = frame_reg_kernel<M, OP>;
+// ---------------------------------------------- TMA tensor maps (driver API)
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        PTG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) raise(PTG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// object n x n complex64 viewed as float32 [n][2n]; box = one M x M window
+void encode_z(CUtensorMap* tm, const void* z, int n, int M) {
+    cuuint64_t dims[2] = {(cuuint64_t)2 * n, (cuuint64_t)n};
+    cuuint64_t strides[1] = {(cuuint64_t)2 * n * sizeof(float)};
+    cuuint32_t box[2] = {(cuuint32_t)2 * M, (cuuint32_t)M};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(z), dims, strides,
+                             box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) raise(PTG_ERR_CUDA, "tensor map (object) encode failed: " + std::to_string((int)r));
+}
+
+// amplitudes float32 [N][M][M]; box = (min(M,32) x M) tile of one pattern, swizzled
+void encode_amp(CUtensorMap* tm, const void* amp, int M, int N) {
+    const int AT = M < 32 ? M : 32;
+    cuuint64_t dims[3] = {(cuuint64_t)M, (cuuint64_t)M, (cuuint64_t)N};
+    cuuint64_t strides[2] = {(cuuint64_t)M * sizeof(float), (cuuint64_t)M * M * sizeof(float)};
+    cuuint32_t box[3] = {(cuuint32_t)AT, (cuuint32_t)M, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = encode_fn()(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(amp), dims, strides,
+                             box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             AT == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) raise(PTG_ERR_CUDA, "tensor map (data) encode failed: " + std::to_string((int)r));
+}
+
+bool tma_path_ok(const Plan& p) {
+    return p.prec == PTG_C64 && (p.M == 16 || p.M == 32 || p.M == 64) && p.w == p.M && p.n % 2 == 0 &&
+           p.N > 0;
+}
+
+template <int M, int OP, bool PROBE>
+void launch_tma_p(const FrameArgs<float>& a, int count, const CUtensorMap& tz, const CUtensorMap& ta,
+                  const CUtensorMap& tp, cudaStream_t s) {
+    constexpr int FPC = tma_frames_per_cta<M>();
+    constexpr size_t smem = tma_smem_bytes<M>();
+    auto kern = frame_tma_kernel<M, OP, PROBE>;
     static bool attr = false;
     if (!attr) {
         PTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    kern<<<(count + FPC - 1) / FPC, M * FPC, smem, s>>>(a, count);
+    kern<<<(count + FPC - 1) / FPC, M * FPC, smem, s>>>(a, count, tz, ta, tp);
     PTG_CHECK_LAUNCH();
 }
 
 template <int OP>
-bool launch_reg(int M, const FrameArgs<float>& a, int count, cudaStream_t s) {
-    switch (M) {
-        case 16: launch_reg_t<16, OP>(a, count, s); return true;
-        case 32: launch_reg_t<32, OP>(a, count, s); return true;
-        case 64: launch_reg_t<64, OP>(a, count, s); return true;
-        default: return false;
+void launch_tma(Plan& p, const FrameArgs<float>& a, int count, const void* z, const float* data) {
+    // cached maps: amplitudes per (buffer, metric); object per pointer (small LRU)
+    if (p.tm_amp_ptr != data) {
+        encode_amp(reinterpret_cast<CUtensorMap*>(p.tm_amp), data, p.M, p.N);
+        p.tm_amp_ptr = data;
+    }
+    CUtensorMap* tz = nullptr;
+    for (auto& e : p.tm_z_cache)
+        if (e.ptr == z) tz = reinterpret_cast<CUtensorMap*>(e.map);
+    if (!tz) {
+        auto& e = p.tm_z_cache[p.tm_z_next++ % p.tm_z_cache.size()];
+        encode_z(reinterpret_cast<CUtensorMap*>(e.map), z, p.n, p.M);
+        e.ptr = z;
+        tz = reinterpret_cast<CUtensorMap*>(e.map);
+    }
+    const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(p.tm_amp);
+    const bool pr = a.probe != nullptr;
+    if (pr && !p.tm_probe_ok) {   // probe M x M complex64 as float32 [M][2M], one box
+        encode_z(reinterpret_cast<CUtensorMap*>(p.tm_probe), a.probe, p.M, p.M);
+        p.tm_probe_ok = true;
+    }
+    const CUtensorMap& tp = pr ? *reinterpret_cast<const CUtensorMap*>(p.tm_probe) : *tz;
+    switch (p.M) {
+        case 16: pr ? launch_tma_p<16, OP, true>(a, count, *tz, ta, tp, p.stream) : launch_tma_p<16, OP, false>(a, count, *tz, ta, tp, p.stream); break;
+        case 32: pr ? launch_tma_p<32, OP, true>(a, count, *tz, ta, tp, p.stream) : launch_tma_p<32, OP, false>(a, count, *tz, ta, tp, p.stream); break;
+        default: pr ? launch_tma_p<64, OP, true>(a, count, *tz, ta, tp, p.stream) : launch_tma_p<64, OP, false>(a, count, *tz, ta, tp, p.stream); break;
     }
 }
 
-// objective frame kernel: register path for complex64 M in {16,32,64}, smem path otherwise
+// objective frame kernel: TMA/register path for complex64 patch frames, smem path otherwise
 template <typename T, int OP>
-void launch_objective(int M, const FrameArgs<T>& a, int count, cudaStream_t s) {
+void launch_objective(Plan& p, const FrameArgs<T>& a, int count, const void* z, const T* data) {
     if constexpr (sizeof(T) == 4) {
-        if (launch_reg<OP>(M, a, count, s)) return;
+        if (tma_path_ok(p)) {
+            launch_tma<OP>(p, a, count, z, data);
+            return;
+        }
     }
-    launch_frame_m<T, OP>(M, a, count, s);
+    launch_frame_m<T, OP>(p.M, a, count, p.stream);
 }
 
 bool frame_supported(int prec, int M) {
@@ -164,6 +233,32 @@ FrameArgs<T> frame_args(Plan& p, const void* z, const T* amp) {
     return a;
 }
 
+// value = sum_j misfit_j - sum_t dotp_t by 256 threads: fixed contiguous
+// partition + fixed shuffle tree + fixed warp order (deterministic)
+__device__ __forceinline__ void finalize_block(const double* misfit, int N, const double* dotp, int ndot,
+                                               double* out, double* red, int lin) {
+    double m = 0.0, d = 0.0;
+    const int cm = (N + 255) / 256, cd = (ndot + 255) / 256;
+    for (int i = lin * cm, e = min(i + cm, N); i < e; ++i) m += __ldcg(misfit + i);
+    for (int i = lin * cd, e = min(i + cd, ndot); i < e; ++i) d += __ldcg(dotp + i);
+    double both[2] = {m, d};
+    double res[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        double x = both[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        __syncthreads();
+        if ((lin & 31) == 0) red[lin >> 5] = x;
+        __syncthreads();
+        double s = 0.0;
+        if (lin == 0)
+            for (int i = 0; i < 8; ++i) s += red[i];
+        res[q] = s;
+    }
+    if (lin == 0) *out = res[0] - res[1];
+}
+
 // --------------------------------------------------------- overlap gather
 template <typename T>
 __global__ void __launch_bounds__(256) k_overlap_gather(
@@ -171,33 +266,53 @@ __global__ void __launch_bounds__(256) k_overlap_gather(
     const int* __restrict__ tile_ids, const int* __restrict__ tile_ptr,
     const int* __restrict__ tile_list, int n, int w, int tiles_x, const cplx<T>* __restrict__ v,
     const cplx<T>* __restrict__ z, cplx<T>* __restrict__ grad, double* __restrict__ dotp,
-    int accumulate) {
+    int accumulate, const double* __restrict__ misfit, int N, double* value_out,
+    unsigned int* counter) {
     __shared__ double red[8];
+    constexpr int LCAP = 256;   // list entries staged per round
+    __shared__ int s_j[LCAP];
+    __shared__ int2 s_p[LCAP];
+    // programmatic dependent launch: everything above overlaps the frame
+    // kernel's tail; wait here until its stash/misfit writes are visible
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int t = tile_ids ? tile_ids[blockIdx.x] : blockIdx.x;
     const int ty = t / tiles_x, tx = t % tiles_x;
     const int x = tx * kTileW + threadIdx.x;
     const int y = ty * kTileH + threadIdx.y;
-    // one pixel per thread; candidate windows fetched U at a time so their
-    // (independent) loads overlap, then added strictly in list (= scan) order
-    constexpr int U = 8;
+    const int lin = threadIdx.y * kTileW + threadIdx.x;
+    // one pixel per thread; the tile's window list (ascending scan order) is
+    // staged in shared memory, stash loads are issued U at a time (independent,
+    // branch-free with clamped addresses) and added strictly in list order
+    constexpr int U = 16;
     cplx<T> acc = mk<T>(T(0), T(0));
     const int e0 = tile_ptr[blockIdx.x], e1 = tile_ptr[blockIdx.x + 1];
-    for (int e = e0; e < e1; e += U) {
-        cplx<T> val[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            val[u] = mk<T>(T(0), T(0));
-            if (e + u < e1) {
-                const int j = __ldg(tile_list + e + u);
-                const int2 p = __ldg(pos + j);
-                const int cx = x - p.y, cy = y - p.x;
-                if ((unsigned)cx < (unsigned)w && (unsigned)cy < (unsigned)w)
-                    val[u] = stash[(size_t)(j - stash_first) * w * w + (size_t)cy * w + cx];
-            }
+    for (int base = e0; base < e1; base += LCAP) {
+        const int cnt = min(LCAP, e1 - base);
+        __syncthreads();
+        for (int i = lin; i < cnt; i += kTileW * kTileH) {
+            const int j = tile_list[base + i];
+            s_j[i] = j - stash_first;
+            s_p[i] = pos[j];
         }
+        __syncthreads();
+        for (int e = 0; e < cnt; e += U) {
+            size_t off[U];
+            bool ok[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (e + u < e1) acc = cadd(acc, val[u]);
+            for (int u = 0; u < U; ++u) {
+                const int i = min(e + u, cnt - 1);
+                const int2 p = s_p[i];
+                const int cx = x - p.y, cy = y - p.x;
+                ok[u] = (e + u < cnt) && (unsigned)cx < (unsigned)w && (unsigned)cy < (unsigned)w;
+                off[u] = (size_t)s_j[i] * w * w + (ok[u] ? (size_t)cy * w + cx : 0);
+            }
+            cplx<T> val[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) val[u] = stash[off[u]];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (ok[u]) acc = cadd(acc, val[u]);
+        }
     }
     double d = 0.0;
     if (x < n && y < n) {
@@ -211,16 +326,29 @@ __global__ void __launch_bounds__(256) k_overlap_gather(
         }
         grad[idx] = g;
     }
-    if (v) {
+    if (v || value_out) {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-        const int lin = threadIdx.y * 32 + threadIdx.x;
         if ((lin & 31) == 0) red[lin >> 5] = d;
         __syncthreads();
         if (lin == 0) {
             double s = 0.0;
             for (int i = 0; i < 8; ++i) s += red[i];
             dotp[blockIdx.x] = s;
+        }
+    }
+    if (value_out) {
+        // fused finalize: the last block to finish reduces misfit + dot partials
+        __shared__ bool last;
+        if (lin == 0) {
+            __threadfence();
+            last = atomicAdd(counter, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            finalize_block(misfit, N, dotp, gridDim.x, value_out, red, lin);
+            if (lin == 0) *counter = 0u;
         }
     }
 }
@@ -249,31 +377,11 @@ __global__ void __launch_bounds__(256) k_shift(const cplx<T>* __restrict__ v, co
     }
 }
 
-// value = sum_j misfit_j - sum_t dotp_t, fixed partition + fixed tree
 __global__ void __launch_bounds__(256) k_finalize(const double* __restrict__ misfit, int N,
                                                   const double* __restrict__ dotp, int ndot,
                                                   double* __restrict__ out) {
     __shared__ double red[8];
-    double m = 0.0, d = 0.0;
-    const int cm = (N + 255) / 256, cd = (ndot + 255) / 256;
-    for (int i = threadIdx.x * cm, e = min(i + cm, N); i < e; ++i) m += misfit[i];
-    for (int i = threadIdx.x * cd, e = min(i + cd, ndot); i < e; ++i) d += dotp[i];
-    double both[2] = {m, d};
-    double res[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        double x = both[q];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
-        __syncthreads();
-        double s = 0.0;
-        if (threadIdx.x == 0)
-            for (int i = 0; i < 8; ++i) s += red[i];
-        res[q] = s;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *out = res[0] - res[1];
+    finalize_block(misfit, N, dotp, ndot, out, red, threadIdx.x);
 }
 
 // --------------------------------------------------------------- data prep
@@ -509,6 +617,8 @@ std::unique_ptr<Plan> plan_create(const ptg_plan_desc& d) {
     }
     build_chunks(*p);
     p->value.alloc(4 * sizeof(double));
+    p->counter.alloc(sizeof(unsigned int) * 4);
+    PTG_CUDA(cudaMemset(p->counter.p, 0, p->counter.bytes));
     p->scratch.alloc((kReduceBlocks + 2) * sizeof(double));
     PTG_CUDA(cudaMemset(p->scratch.p, 0, p->scratch.bytes));
     p->flag.alloc(sizeof(unsigned long long));
@@ -593,7 +703,6 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
     const T* data = metric == PTG_DISTANCE ? p.amp.as<const T>() : p.inten.as<const T>();
     const bool single = p.chunks.size() == 1;
     if (!single) dev_fill_zero(p.prec, grad, p.nn(), p.stream);
-    int ndot = 0;
     for (auto& cp : p.chunks) {
         Chunk& c = *cp;
         if (c.count > 0) {
@@ -602,26 +711,38 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
             // frame_kernel writes stash[j*w*w]; offset the base so j - first maps to 0
             a.stash = reinterpret_cast<C*>(p.stash.as<C>()) - (size_t)c.first * p.w * p.w;
             p.ev_begin(0);
-            if (metric == PTG_DISTANCE) launch_objective<T, OP_DISTANCE>(p.M, a, c.count, p.stream);
-            else launch_objective<T, OP_INTENSITY>(p.M, a, c.count, p.stream);
+            if (metric == PTG_DISTANCE) launch_objective<T, OP_DISTANCE>(p, a, c.count, z, data);
+            else launch_objective<T, OP_INTENSITY>(p, a, c.count, z, data);
             p.ev_end();
             ++p.launches;
         }
         if (c.ntiles > 0) {
-            dim3 blk(32, 8);
+            // single-chunk plans fuse the shift, <v,z> and the final value reduction
+            // into the gather (last-block-done); it is chained to the frame kernel
+            // by programmatic dependent launch so its launch overlaps the frame tail
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(c.ntiles);
+            cfg.blockDim = dim3(kTileW, kTileH);
+            cfg.stream = p.stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = p.timing ? 0 : 1;   // event timing needs plain kernel boundaries
             p.ev_begin(1);
-            k_overlap_gather<T><<<c.ntiles, blk, 0, p.stream>>>(
-                p.stash.as<const C>(), c.first, p.pos.as<const int2>(),
-                c.all_tiles ? nullptr : c.tile_ids.as<const int>(), c.tile_ptr.as<const int>(),
+            PTG_CUDA(cudaLaunchKernelEx(
+                &cfg, k_overlap_gather<T>, p.stash.as<const C>(), c.first, p.pos.as<const int2>(),
+                c.all_tiles ? (const int*)nullptr : c.tile_ids.as<const int>(), c.tile_ptr.as<const int>(),
                 c.tile_list.as<const int>(), p.n, p.w, p.tiles_x,
-                single ? static_cast<const C*>(v) : nullptr, static_cast<const C*>(z),
-                static_cast<C*>(grad), p.dotp.as<double>(), single ? 0 : 1);
-            PTG_CHECK_LAUNCH();
+                single ? static_cast<const C*>(v) : (const C*)nullptr, static_cast<const C*>(z),
+                static_cast<C*>(grad), p.dotp.as<double>(), single ? 0 : 1, p.misfit.as<const double>(),
+                p.N, single ? value_dev : (double*)nullptr, p.counter.as<unsigned int>()));
             p.ev_end();
             ++p.launches;
-            if (single && v) ndot = c.ntiles;
         }
     }
+    if (single && p.chunks[0]->ntiles > 0) return;   // value produced by the fused gather
+    int ndot = 0;
     if (!single && v) {
         const int blocks = 1024;
         k_shift<T><<<blocks, 256, 0, p.stream>>>(static_cast<const C*>(v), static_cast<const C*>(z),

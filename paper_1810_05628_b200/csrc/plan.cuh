@@ -79,6 +79,7 @@ struct Plan {
     bool amp_valid = false, inten_valid = false;
 
     DevMem stash, misfit, dotp, value, scratch, flag, frame;
+    DevMem counter;                  // last-block-done counter of the fused gather
     DevMem zbuf, vbuf, gbuf, stage;  // host-API working buffers
     HostPinned hval;
 
@@ -90,6 +91,15 @@ struct Plan {
     void ev_begin(int kind);
     void ev_end();
     void timing_collect(double* ms, int64_t* cnt);   // ms[2], cnt[2]
+
+    // TMA tensor maps (opaque 128-B CUtensorMap blobs) for the complex64 fast path
+    alignas(64) unsigned char tm_amp[128] = {};
+    const void* tm_amp_ptr = nullptr;
+    alignas(64) unsigned char tm_probe[128] = {};
+    bool tm_probe_ok = false;
+    struct TmEntry { const void* ptr = nullptr; alignas(64) unsigned char map[128] = {}; };
+    std::vector<TmEntry> tm_z_cache = std::vector<TmEntry>(8);
+    size_t tm_z_next = 0;
 
     int tiles_x = 0, tiles_y = 0;
     int chunk_size = 0;
