@@ -346,9 +346,12 @@ class Hierarchy:
         self.depth = depth
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().ptgo_hierarchy_free(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                lib().ptgo_hierarchy_free(self._h)
+                self._h = None
+        except Exception:
+            pass
 
     def level(self, l: int) -> Problem:
         L = lib()

@@ -69,24 +69,25 @@ __device__ __forceinline__ void dft4(C& a0, C& a1, C& a2, C& a3) {
     a3 = csub(t1, t3);
 }
 
-// (x + iy) * W8^1 (forward W8 = (1 - i)/sqrt2; inverse conj)
+// (x + iy) * W8^1 (forward W8 = (1 - i)/sqrt2; inverse conj), written as a
+// complex add of the swapped/negated copy so packed FP32 folds it to 2 ops
 template <bool INV, typename C>
 __device__ __forceinline__ C mul_w8_1(C a) {
     using T = decltype(a.x);
     const T c = T(0.70710678118654752440084436210485);
-    C r;
-    if (INV) { r.x = c * (a.x - a.y); r.y = c * (a.x + a.y); }
-    else     { r.x = c * (a.x + a.y); r.y = c * (a.y - a.x); }
-    return r;
+    C sw;
+    if (INV) { sw.x = -a.y; sw.y = a.x; }   // (x - y, y + x)
+    else     { sw.x = a.y; sw.y = -a.x; }   // (x + y, y - x)
+    return cscale(cadd(a, sw), c);
 }
 template <bool INV, typename C>
 __device__ __forceinline__ C mul_w8_3(C a) {   // W8^3 = (-1 - i)/sqrt2 forward
     using T = decltype(a.x);
     const T c = T(0.70710678118654752440084436210485);
-    C r;
-    if (INV) { r.x = -c * (a.x + a.y); r.y = c * (a.x - a.y); }
-    else     { r.x = c * (a.y - a.x); r.y = -c * (a.x + a.y); }
-    return r;
+    C sw;
+    if (INV) { sw.x = -a.y; sw.y = a.x; }   // (-y - x, x - y)
+    else     { sw.x = a.y; sw.y = -a.x; }   // (y - x, -x - y)
+    return cscale(csub(sw, a), c);
 }
 
 template <bool INV, typename C>

@@ -124,7 +124,7 @@ __device__ __forceinline__ float2 twiddle_mul(float2 v) {
     } else {
         constexpr float c = (float)ct_cos(ct_angle(e, L));
         constexpr float s = INV ? (float)ct_sin(ct_angle(e, L)) : -(float)ct_sin(ct_angle(e, L));
-        return make_float2(v.x * c - v.y * s, v.x * s + v.y * c);
+        return cmul(make_float2(c, s), v);   // FMUL2 + FFMA2 with immediate operands
     }
 }
 

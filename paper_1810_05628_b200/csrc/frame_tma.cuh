@@ -81,9 +81,10 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
     const int jl = blockIdx.x * FPC + f;
     const bool live = jl < count;
     const int j = a.first + (live ? jl : 0);
-    unsigned char* base = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(smem_tma) + 1023) & ~uintptr_t(1023));
-    unsigned char* fr = base + (size_t)f * tma_frame_bytes<M>();
+    // 1 KiB-align inside the dynamic buffer by offsetting the shared array itself
+    // (keeps the shared address space visible to the compiler: LDS/STS, not LD/ST)
+    const uint32_t pad = (1024u - (smem_u32(smem_tma) & 1023u)) & 1023u;
+    unsigned char* fr = smem_tma + pad + (size_t)f * tma_frame_bytes<M>();
     float2* buf = reinterpret_cast<float2*>(fr);
 
     if (t == 0) {

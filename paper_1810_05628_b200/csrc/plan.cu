@@ -262,69 +262,73 @@ __device__ __forceinline__ void finalize_block(const double* misfit, int N, cons
 // --------------------------------------------------------- overlap gather
 template <typename T>
 __global__ void __launch_bounds__(256) k_overlap_gather(
-    const cplx<T>* __restrict__ stash, int stash_first, const int2* __restrict__ pos,
-    const int* __restrict__ tile_ids, const int* __restrict__ tile_ptr,
-    const int* __restrict__ tile_list, int n, int w, int tiles_x, const cplx<T>* __restrict__ v,
+    const cplx<T>* __restrict__ stash, const int* __restrict__ tile_ids,
+    const int* __restrict__ tile_ptr, const int4* __restrict__ entries, int n, int w, int tiles_x,
+    const cplx<T>* __restrict__ v,
     const cplx<T>* __restrict__ z, cplx<T>* __restrict__ grad, double* __restrict__ dotp,
     int accumulate, const double* __restrict__ misfit, int N, double* value_out,
     unsigned int* counter) {
     __shared__ double red[8];
-    constexpr int LCAP = 256;   // list entries staged per round
-    __shared__ int s_j[LCAP];
-    __shared__ int2 s_p[LCAP];
+    constexpr int PPT = kTileH / 8;   // pixels (rows) per thread
     // programmatic dependent launch: everything above overlaps the frame
     // kernel's tail; wait here until its stash/misfit writes are visible
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int t = tile_ids ? tile_ids[blockIdx.x] : blockIdx.x;
     const int ty = t / tiles_x, tx = t % tiles_x;
     const int x = tx * kTileW + threadIdx.x;
-    const int y = ty * kTileH + threadIdx.y;
+    const int y0 = ty * kTileH + threadIdx.y;
     const int lin = threadIdx.y * kTileW + threadIdx.x;
-    // one pixel per thread; the tile's window list (ascending scan order) is
-    // staged in shared memory, stash loads are issued U at a time (independent,
-    // branch-free with clamped addresses) and added strictly in list order
-    constexpr int U = 16;
-    cplx<T> acc = mk<T>(T(0), T(0));
-    const int e0 = tile_ptr[blockIdx.x], e1 = tile_ptr[blockIdx.x + 1];
-    for (int base = e0; base < e1; base += LCAP) {
-        const int cnt = min(LCAP, e1 - base);
-        __syncthreads();
-        for (int i = lin; i < cnt; i += kTileW * kTileH) {
-            const int j = tile_list[base + i];
-            s_j[i] = j - stash_first;
-            s_p[i] = pos[j];
-        }
-        __syncthreads();
-        for (int e = 0; e < cnt; e += U) {
-            size_t off[U];
-            bool ok[U];
+    // PPT pixels per thread (rows y0 + 8i).  The tile's windows (ascending scan
+    // order, host-precomputed as {stash offset - r0*w - c0, r0, c0}) are read
+    // with warp-uniform 16-B loads; per pixel an add, a compare and a
+    // predicated stash load; U entries in flight; adds strictly in list order
+    // (the reference's accumulation order)
+    constexpr int U = 8;
+    cplx<T> acc[PPT];
+    int pix[PPT];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int i = min(e + u, cnt - 1);
-                const int2 p = s_p[i];
-                const int cx = x - p.y, cy = y - p.x;
-                ok[u] = (e + u < cnt) && (unsigned)cx < (unsigned)w && (unsigned)cy < (unsigned)w;
-                off[u] = (size_t)s_j[i] * w * w + (ok[u] ? (size_t)cy * w + cx : 0);
+    for (int i = 0; i < PPT; ++i) {
+        acc[i] = mk<T>(T(0), T(0));
+        pix[i] = (y0 + 8 * i) * w + x;
+    }
+    const int e0 = tile_ptr[blockIdx.x], cnt = tile_ptr[blockIdx.x + 1] - e0;
+    const int4* __restrict__ E = entries + e0;
+    for (int e = 0; e < cnt; e += U) {
+        int4 en[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) en[u] = __ldg(E + min(e + u, cnt - 1));
+        cplx<T> val[U][PPT];
+        bool ok[U][PPT];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool inx = (e + u < cnt) && (unsigned)(x - en[u].z) < (unsigned)w;
+#pragma unroll
+            for (int i = 0; i < PPT; ++i) {
+                ok[u][i] = inx && (unsigned)(y0 + 8 * i - en[u].y) < (unsigned)w;
+                val[u][i] = ok[u][i] ? stash[en[u].x + pix[i]] : mk<T>(T(0), T(0));
             }
-            cplx<T> val[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) val[u] = stash[off[u]];
-#pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (ok[u]) acc = cadd(acc, val[u]);
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int i = 0; i < PPT; ++i)
+                if (ok[u][i]) acc[i] = cadd(acc[i], val[u][i]);
     }
     double d = 0.0;
-    if (x < n && y < n) {
-        const size_t idx = (size_t)y * n + x;
-        cplx<T> g = acc;
-        if (accumulate) g = cadd(grad[idx], g);
-        if (v) {
-            const cplx<T> vv = v[idx], zz = z[idx];
-            g = csub(g, vv);
-            d = (double)vv.x * (double)zz.x + (double)vv.y * (double)zz.y;
+#pragma unroll
+    for (int i = 0; i < PPT; ++i) {
+        const int y = y0 + 8 * i;
+        if (x < n && y < n) {
+            const size_t idx = (size_t)y * n + x;
+            cplx<T> g = acc[i];
+            if (accumulate) g = cadd(grad[idx], g);
+            if (v) {
+                const cplx<T> vv = v[idx], zz = z[idx];
+                g = csub(g, vv);
+                d += (double)vv.x * (double)zz.x + (double)vv.y * (double)zz.y;
+            }
+            grad[idx] = g;
         }
-        grad[idx] = g;
     }
     if (v || value_out) {
 #pragma unroll
@@ -530,12 +534,17 @@ void build_chunks(Plan& p) {
             for (int ty = ty0; ty <= ty1; ++ty)
                 for (int tx = tx0; tx <= tx1; ++tx) lists[ty * p.tiles_x + tx].push_back(j);
         }
-        std::vector<int> ids, ptr{0}, list;
+        std::vector<int> ids, ptr{0};
+        std::vector<int4> list;   // {stash offset of window origin - r0*w - c0, r0, c0, j}
         c->all_tiles = (nchunks == 1);
         for (int t = 0; t < ntiles; ++t) {
             if (!c->all_tiles && lists[t].empty()) continue;
             ids.push_back(t);
-            list.insert(list.end(), lists[t].begin(), lists[t].end());
+            for (int j : lists[t]) {
+                const int r0 = p.pos_h[2 * j], c0 = p.pos_h[2 * j + 1];
+                const long long off = (long long)(j - c->first) * p.w * p.w - (long long)r0 * p.w - c0;
+                list.push_back(make_int4((int)off, r0, c0, j));
+            }
             ptr.push_back((int)list.size());
         }
         c->ntiles = (int)ids.size();
@@ -545,8 +554,9 @@ void build_chunks(Plan& p) {
         }
         c->tile_ptr.alloc(ptr.size() * sizeof(int));
         PTG_CUDA(cudaMemcpy(c->tile_ptr.p, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
-        c->tile_list.alloc(std::max<size_t>(1, list.size()) * sizeof(int));
-        if (!list.empty()) PTG_CUDA(cudaMemcpy(c->tile_list.p, list.data(), list.size() * sizeof(int), cudaMemcpyHostToDevice));
+        // int32 stash offsets: the per-chunk stash budget keeps them < 2^31 elements
+        c->tile_list.alloc(std::max<size_t>(1, list.size()) * sizeof(int4));
+        if (!list.empty()) PTG_CUDA(cudaMemcpy(c->tile_list.p, list.data(), list.size() * sizeof(int4), cudaMemcpyHostToDevice));
         p.chunks.push_back(std::move(c));
     }
     p.stash.alloc(std::max<size_t>(1, (size_t)cs * p.w * p.w) * p.celem());
@@ -722,7 +732,7 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
             // by programmatic dependent launch so its launch overlaps the frame tail
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(c.ntiles);
-            cfg.blockDim = dim3(kTileW, kTileH);
+            cfg.blockDim = dim3(kTileW, 8);
             cfg.stream = p.stream;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -731,9 +741,9 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
             cfg.numAttrs = p.timing ? 0 : 1;   // event timing needs plain kernel boundaries
             p.ev_begin(1);
             PTG_CUDA(cudaLaunchKernelEx(
-                &cfg, k_overlap_gather<T>, p.stash.as<const C>(), c.first, p.pos.as<const int2>(),
+                &cfg, k_overlap_gather<T>, p.stash.as<const C>(),
                 c.all_tiles ? (const int*)nullptr : c.tile_ids.as<const int>(), c.tile_ptr.as<const int>(),
-                c.tile_list.as<const int>(), p.n, p.w, p.tiles_x,
+                c.tile_list.as<const int4>(), p.n, p.w, p.tiles_x,
                 single ? static_cast<const C*>(v) : (const C*)nullptr, static_cast<const C*>(z),
                 static_cast<C*>(grad), p.dotp.as<double>(), single ? 0 : 1, p.misfit.as<const double>(),
                 p.N, single ? value_dev : (double*)nullptr, p.counter.as<unsigned int>()));

@@ -62,8 +62,8 @@ struct Chunk {
     DevMem tile_ids, tile_ptr, tile_list;
 };
 
-constexpr int kTileW = 32;   // overlap-add gather tile: 32 x 8 pixels, one per thread
-constexpr int kTileH = 8;
+constexpr int kTileW = 32;   // overlap-add gather tile: 32 x 16 pixels, 2 per thread (32 x 8 block)
+constexpr int kTileH = 16;
 
 struct Plan {
     int n = 0, M = 0, w = 0, N = 0, prec = PTG_C64, device = 0;

@@ -268,6 +268,22 @@ class Hierarchy:
         return SolverReport(z, rep.final_value, h, STOP_NAMES[rep.reason], rep.weighted,
                             [int(rep.per_level[l]) for l in range(self.depth)])
 
+    def level(self, l: int) -> "Plan":
+        """Non-owning Plan view of hierarchy level l (0 = the fine plan)."""
+        h = C.c_void_p()
+        check(lib().ptg_hier_level(self._h, int(l), C.byref(h)))
+        if l == 0:
+            return self.plan
+        v = Plan.__new__(Plan)
+        n, M, w, N = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        check(lib().ptg_plan_info(h, C.byref(n), C.byref(M), C.byref(w), C.byref(N), None, None))
+        v.n, v.M, v.w, v.N = n.value, M.value, w.value, N.value
+        v.precision = self.plan.precision
+        v._h = h
+        v._view_of = self   # keep the hierarchy alive; never destroyed through the view
+        v.close = lambda: None
+        return v
+
     def cycle_device(self, z, grad, value: float):
         """One top-level V-cycle in place on device tensors (z, grad); returns
         (new value, weighted evals, per-level eval counts)."""

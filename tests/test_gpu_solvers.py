@@ -1,0 +1,158 @@
+"""GPU-resident solvers vs the reference (golden vectors) and the oracle.
+
+complex128: trajectory-level parity (identical per-level evaluation counts and
+stop reasons, histories / iterates within 1e-9..1e-10 relative).  complex64:
+per-sweep / per-eval tolerances (discrete line-search decisions may flip in
+fp32, so counts are only required to match in c128; SURVEY.md 7 hard part 7).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import rand_field, rel_l2
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz")
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return dict(np.load(GOLD))
+
+
+def _ref_plan(gold, precision="c128"):
+    from paper_1810_05628_b200 import Plan
+    n, w, s = (int(v) for v in gold["eval_b_geom"])
+    return Plan(n, n, w, gold["eval_b_pos"], gold["eval_b_data"], None, precision=precision), n, w, s
+
+
+def test_pie_ref_mode_vs_reference(gold):
+    plan, n, w, s = _ref_plan(gold)
+    r = plan.pie(gold["pie_z0"], gamma=0.1, sweeps=3)
+    assert rel_l2(r.final_iterate, gold["pie_z"]) <= 1e-10
+    np.testing.assert_allclose(r.history, gold["pie_hist"], rtol=1e-10, atol=1e-12)
+    assert r.weighted_evals == gold["pie_meta"][1]
+
+
+def test_lbfgs_ref_mode_vs_reference(gold):
+    plan, n, w, s = _ref_plan(gold)
+    r = plan.lbfgs(gold["pie_z0"], v=gold["eval_b_v"], max_iters=6)
+    assert r.history.shape == gold["lbfgs_hist"].shape
+    np.testing.assert_allclose(r.history[:, 0], gold["lbfgs_hist"][:, 0], rtol=0)   # identical eval counts
+    np.testing.assert_allclose(r.history[:, 1:], gold["lbfgs_hist"][:, 1:], rtol=1e-9)
+    assert rel_l2(r.final_iterate, gold["lbfgs_z"]) <= 1e-9
+
+
+@pytest.mark.parametrize("depth", [2, 3])
+def test_mgopt_ref_mode_vs_reference(gold, depth):
+    from paper_1810_05628_b200 import Hierarchy
+    plan, n, w, s = _ref_plan(gold)
+    h = Hierarchy(plan, depth, coarsest_max_iters=10)
+    r = h.driver(gold[f"mg{depth}_z0"], budget=1e9, max_cycles=3)
+    meta = gold[f"mg{depth}_meta"]
+    assert r.per_level_evals == [int(x) for x in meta[3:]]
+    assert r.weighted_evals == meta[1]
+    np.testing.assert_allclose(r.history, gold[f"mg{depth}_hist"], rtol=1e-9)
+    assert rel_l2(r.final_iterate, gold[f"mg{depth}_z"]) <= 1e-9
+
+
+def _patch(oracle, precision, cfg=None):
+    from paper_1810_05628_b200 import Plan, synth
+    cfg = cfg or synth.small_config(precision=precision)
+    obj, probe, pos = synth.make_inputs(cfg)
+    if precision == "c64":
+        obj = obj.astype(np.complex64).astype(np.complex128)
+        probe = probe.astype(np.complex64).astype(np.complex128)
+    data = oracle.simulate(cfg.n, cfg.M, cfg.w, pos, obj, probe)
+    if precision == "c64":
+        data = data.astype(np.float32)
+    p = oracle.Problem(cfg.n, cfg.M, cfg.w, pos, data.astype(np.float64), probe)
+    plan = Plan(cfg.n, cfg.M, cfg.w, pos, data, probe, precision=precision)
+    return p, plan, cfg
+
+
+def test_pie_patch_c128_vs_oracle(oracle):
+    p, plan, cfg = _patch(oracle, "c128")
+    z0 = np.ones((cfg.n, cfg.n), np.complex128)
+    want = oracle.pie(p, z0, 0.05, 2)
+    got = plan.pie(z0, gamma=0.05, sweeps=2)
+    assert rel_l2(got.final_iterate, want.z) <= 1e-10
+    np.testing.assert_allclose(got.history, want.history, rtol=1e-10)
+
+
+def test_pie_config2_c64_vs_oracle(oracle):
+    from paper_1810_05628_b200 import synth
+    p, plan, cfg = _patch(oracle, "c64", synth.CONFIGS[2])
+    z0 = np.ones((cfg.n, cfg.n), np.complex128)
+    want = oracle.pie(p, z0, 0.0, 1)
+    got = plan.pie(z0, gamma=0.0, sweeps=1)
+    # 841 strictly sequential fp32 projections: per-projection rounding (~1e-6)
+    # accumulates along the sweep, so the iterate tolerance is 3e-4 while the
+    # objective values stay within the 1e-5 complex64 bar
+    assert rel_l2(got.final_iterate, want.z) <= 3e-4
+    np.testing.assert_allclose(got.history[:, 1], want.history[:, 1], rtol=1e-5)
+
+
+def test_mgopt_patch_c128_vs_oracle(oracle):
+    from paper_1810_05628_b200 import Hierarchy
+    p, plan, cfg = _patch(oracle, "c128")
+    z0 = np.ones((cfg.n, cfg.n), np.complex128)
+    want = oracle.Hierarchy(p, 2).driver(z0, budget=1e9, max_cycles=3)
+    got = Hierarchy(plan, 2).driver(z0, budget=1e9, max_cycles=3)
+    assert got.per_level_evals == want.per_level
+    np.testing.assert_allclose(got.history, want.history, rtol=1e-8)
+    assert rel_l2(got.final_iterate, want.z) <= 1e-8
+
+
+def test_mgopt_config1_c64_values(oracle):
+    """Config-1 geometry in complex64: values track the c128 oracle to 1e-4."""
+    from paper_1810_05628_b200 import Hierarchy, synth
+    cfg = synth.Config(1, 128, 32, 13, 8, 4.0, 8.0, 0.01, "c64", depth=2)
+    p, plan, cfg = _patch(oracle, "c64", cfg)
+    z0 = np.ones((cfg.n, cfg.n), np.complex128)
+    want = oracle.Hierarchy(p, 2).driver(z0, budget=1e9, max_cycles=2)
+    got = Hierarchy(plan, 2).driver(z0, budget=1e9, max_cycles=2)
+    assert got.history.shape == want.history.shape
+    np.testing.assert_allclose(got.history[:, 1], want.history[:, 1], rtol=1e-4)
+
+
+def test_mgopt_deterministic(oracle):
+    from paper_1810_05628_b200 import Hierarchy
+    p, plan, cfg = _patch(oracle, "c64")
+    z0 = np.ones((cfg.n, cfg.n), np.complex128)
+    h = Hierarchy(plan, 2)
+    a = h.driver(z0, budget=1e9, max_cycles=2)
+    b = h.driver(z0, budget=1e9, max_cycles=2)
+    assert np.array_equal(a.final_iterate, b.final_iterate)
+    assert np.array_equal(a.history, b.history)
+
+
+def test_depth1_is_lbfgs(oracle):
+    """multigrid.cpp:185-189: depth-1 hierarchy == plain LBFGS (bitwise)."""
+    from paper_1810_05628_b200 import Hierarchy
+    p, plan, cfg = _patch(oracle, "c128")
+    z0 = np.ones((cfg.n, cfg.n), np.complex128)
+    a = Hierarchy(plan, 1).driver(z0, budget=1e9, max_cycles=3)
+    b = plan.lbfgs(z0, max_iters=3)
+    assert np.array_equal(a.final_iterate, b.final_iterate)
+    assert np.array_equal(a.history, b.history)
+
+
+def test_hierarchy_errors():
+    from paper_1810_05628_b200 import ConfigError, Hierarchy, Plan
+    n = 16
+    plan = Plan(n, n, 8, np.array([[0, 0], [4, 4]], np.int32), np.ones((2, n, n)), None, precision="c128")
+    with pytest.raises(ConfigError):
+        Hierarchy(plan, 3)   # would coarsen below 8
+    with pytest.raises(ConfigError):
+        Hierarchy(plan, 0)
+
+
+def test_lbfgs_budget_and_stall(oracle):
+    p, plan, cfg = _patch(oracle, "c128")
+    z0 = np.ones((cfg.n, cfg.n), np.complex128)
+    r = plan.lbfgs(z0, max_iters=50, max_weighted=5.0)
+    assert r.reason == "budget" and r.weighted_evals >= 5.0
+    w = oracle.lbfgs(p, z0, max_iters=50, max_weighted=5.0)
+    assert r.weighted_evals == w.weighted

@@ -1,0 +1,68 @@
+"""Multi-rank host logic on CPU (gloo, world size 2): position sharding + the
+gradient/misfit allreduce reproduce the single-process objective.  The
+per-shard evaluator here is the CPU oracle (test infrastructure); on the GPU
+box the same code path runs libptg + NCCL (bench.py)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import ptgo
+        from paper_1810_05628_b200 import sharding, synth
+        cfg = synth.small_config(n=64, M=16, steps=7, step=8)
+        obj, probe, pos = synth.make_inputs(cfg)
+        data = ptgo.simulate(cfg.n, cfg.M, cfg.w, pos, obj, probe)
+        z = np.ones((cfg.n, cfg.n), np.complex128)
+        sp, (a, b) = sharding.shard_positions(pos, cfg.steps, world, rank)
+        val, g = ptgo.evaluate(ptgo.Problem(cfg.n, cfg.M, cfg.w, sp, data[a:b], probe), z)
+        gt = torch.from_numpy(g.copy())
+        val, gt = sharding.allreduce_eval(val, gt)
+        if rank == 0:
+            full = ptgo.evaluate(ptgo.Problem(cfg.n, cfg.M, cfg.w, pos, data, probe), z)
+            q.put((val, full[0], float(np.linalg.norm(gt.numpy() - full[1]) / np.linalg.norm(full[1])),
+                   (a, b)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_blocks_cover_scan():
+    from paper_1810_05628_b200 import sharding
+    for rows in (1, 7, 29, 166):
+        for world in (1, 2, 4, 8):
+            spans = [sharding.row_block(rows, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == rows
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+
+
+@pytest.mark.timeout(120)
+def test_two_rank_allreduce_matches_single_process():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(90)
+    assert all(p.exitcode == 0 for p in ps)
+    val, full_val, grad_rel, span = q.get(timeout=5)
+    assert abs(val - full_val) <= 1e-12 * abs(full_val)
+    assert grad_rel <= 1e-12
