@@ -87,15 +87,19 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
     unsigned char* fr = smem_tma + pad + (size_t)f * tma_frame_bytes<M>();
     float2* buf = reinterpret_cast<float2*>(fr);
 
+    // The object window is loaded as an M x (M+2) box starting at the even
+    // column below col0 (TMA box starts must be 16-B aligned); the tile pitch
+    // is then S and column t of the window sits at t + (col0 & 1).
+    const int2 pj = a.pos[j];
+    const int odd = pj.y & 1;
     if (t == 0) {
         mbar_init(&bar_z[f], 1);
         mbar_init(&bar_a[f], 1);
         mbar_init(&bar_p[f], 1);
         fence_mbarrier_init();
-        if (live) {   // object window -> dense [M][2M floats] tile
-            const int2 p = a.pos[j];
-            mbar_arrive_expect_tx(&bar_z[f], M * M * sizeof(float2));
-            tma_load_2d(fr, &tm_z, 2 * p.y, p.x, &bar_z[f]);
+        if (live) {   // object window -> [M][S] tile (out-of-range columns zero-filled)
+            mbar_arrive_expect_tx(&bar_z[f], M * S * sizeof(float2));
+            tma_load_2d(fr, &tm_z, 2 * (pj.y - odd), pj.x, &bar_z[f]);
         }
     }
 
@@ -110,9 +114,9 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
     __syncthreads();
     if (live) mbar_wait(&bar_z[f], 0);
 #pragma unroll
-    for (int r = 0; r < M; ++r) {   // psi = P o x, own column t (dense pitch M)
-        if constexpr (PROBE) x[r] = cmul(x[r], buf[r * M + t]);
-        else x[r] = buf[r * M + t];
+    for (int r = 0; r < M; ++r) {   // psi = P o x, own column t
+        if constexpr (PROBE) x[r] = cmul(x[r], buf[r * S + t + odd]);
+        else x[r] = buf[r * S + t + odd];
     }
     __syncthreads();
 

@@ -127,11 +127,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// object n x n complex64 viewed as float32 [n][2n]; box = one M x M window
-void encode_z(CUtensorMap* tm, const void* z, int n, int M) {
+// n x n complex64 viewed as float32 [n][2n]; box = M rows x (M + extra) complex
+// (the object window uses extra = 2 so its start can be rounded down to an even
+// column: TMA box starts must be 16-B aligned)
+void encode_z(CUtensorMap* tm, const void* z, int n, int M, int extra) {
     cuuint64_t dims[2] = {(cuuint64_t)2 * n, (cuuint64_t)n};
     cuuint64_t strides[1] = {(cuuint64_t)2 * n * sizeof(float)};
-    cuuint32_t box[2] = {(cuuint32_t)2 * M, (cuuint32_t)M};
+    cuuint32_t box[2] = {(cuuint32_t)(2 * (M + extra)), (cuuint32_t)M};
     cuuint32_t es[2] = {1, 1};
     CUresult r = encode_fn()(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(z), dims, strides,
                              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -185,14 +187,14 @@ void launch_tma(Plan& p, const FrameArgs<float>& a, int count, const void* z, co
         if (e.ptr == z) tz = reinterpret_cast<CUtensorMap*>(e.map);
     if (!tz) {
         auto& e = p.tm_z_cache[p.tm_z_next++ % p.tm_z_cache.size()];
-        encode_z(reinterpret_cast<CUtensorMap*>(e.map), z, p.n, p.M);
+        encode_z(reinterpret_cast<CUtensorMap*>(e.map), z, p.n, p.M, 2);
         e.ptr = z;
         tz = reinterpret_cast<CUtensorMap*>(e.map);
     }
     const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(p.tm_amp);
     const bool pr = a.probe != nullptr;
     if (pr && !p.tm_probe_ok) {   // probe M x M complex64 as float32 [M][2M], one box
-        encode_z(reinterpret_cast<CUtensorMap*>(p.tm_probe), a.probe, p.M, p.M);
+        encode_z(reinterpret_cast<CUtensorMap*>(p.tm_probe), a.probe, p.M, p.M, 0);
         p.tm_probe_ok = true;
     }
     const CUtensorMap& tp = pr ? *reinterpret_cast<const CUtensorMap*>(p.tm_probe) : *tz;

@@ -66,6 +66,17 @@ def test_frame_sizes(oracle, precision, tv, tg, M):
     assert rel_l2(gg, wg) <= tg
 
 
+@pytest.mark.parametrize("M", [16, 32, 64])
+def test_odd_positions_c64(oracle, M):
+    """Jittered scans put windows at odd columns/rows (TMA box starts that are
+    not 16-B aligned)."""
+    from paper_1810_05628_b200 import synth
+    cfg = synth.Config(0, 4 * M + 6, M, 5, M // 2 + 1, 3.0, M / 4, 0.01, "c64", jitter=2)
+    gv, gg, wv, wg, _, _ = _patch_case(oracle, cfg, "c64")
+    assert rel(gv, wv) <= C64_VAL
+    assert rel_l2(gg, wg) <= C64_GRAD
+
+
 def test_frame_128_c64(oracle):
     from paper_1810_05628_b200 import synth
     cfg = synth.Config(0, 256, 128, 3, 64, 6.0, 32.0, 0.0, "c64", jitter=2)
