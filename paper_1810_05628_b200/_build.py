@@ -80,7 +80,28 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
+    build_cpp_tests()
     return LIB
+
+
+CPP = os.path.join(PKG, "cpp")
+CPP_TEST = os.path.join(LIBDIR, "test_ptycho_b200")
+
+
+def build_cpp_tests() -> str:
+    """Reference-style C++ tests of the drop-in header, linked against libptg.so."""
+    src = os.path.join(CPP, "test_shim.cpp")
+    deps = [src, os.path.join(CPP, "ptycho_b200.hpp"), os.path.join(ROOT, "include", "ptg.h"), LIB]
+    if not _stale(CPP_TEST, deps):
+        return CPP_TEST
+    gxx = shutil.which("g++", path="/usr/bin") or "g++"
+    cmd = [gxx, "-std=c++20", "-O2", "-Wall", "-I" + os.path.join(ROOT, "include"), "-I" + CPP, src,
+           "-o", CPP_TEST, "-L" + LIBDIR, "-lptg", "-Wl,-rpath,$ORIGIN"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("C++ drop-in test build failed")
+    return CPP_TEST
 
 
 if __name__ == "__main__":
