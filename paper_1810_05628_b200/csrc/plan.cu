@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 
 #include "frame_kernels.cuh"
+#include "frame_multipass.cuh"
 #include "frame_tma.cuh"
 #include "plan.cuh"
 #include "transfer.cuh"
@@ -217,8 +218,47 @@ void launch_objective(Plan& p, const FrameArgs<T>& a, int count, const void* z, 
     launch_frame_m<T, OP>(p.M, a, count, p.stream);
 }
 
-bool frame_supported(int prec, int M) {
+// single-CTA frame kernels (whole frame in shared memory / registers)
+bool frame_single_cta(int prec, int M) {
     return is_pow2(M) && (M <= 64 || (M == 128 && prec == PTG_C64));
+}
+bool frame_supported(int prec, int M) { return is_pow2(M) && M <= 512 && (frame_single_cta(prec, M) || M >= 128); }
+
+// ------------------------------------------------------- multi-pass frames
+template <typename T, int M, int OP>
+void launch_mp_t(Plan& p, const FrameArgs<T>& a, int first, int count, int which) {
+    constexpr size_t smem = mp_smem_bytes<T, M>();
+    constexpr int NT = mp_threads<M>();
+    static bool attr = false;
+    if (!attr) {
+        PTG_CUDA(cudaFuncSetAttribute(mp_rows_fwd<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        PTG_CUDA(cudaFuncSetAttribute(mp_cols<T, M, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if constexpr (OP != OP_SIMULATE)
+            PTG_CUDA(cudaFuncSetAttribute(mp_rows_inv<T, M, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    MpArgs m{first, M / kMpLines, p.misfit.as<double>()};
+    cplx<T>* scratch = p.mp_scratch.as<cplx<T>>();
+    const dim3 grid(count, M / kMpLines);
+    if (which & 1) { mp_rows_fwd<T, M><<<grid, NT, smem, p.stream>>>(a, m, scratch); PTG_CHECK_LAUNCH(); ++p.launches; }
+    if (which & 2) { mp_cols<T, M, OP><<<grid, NT, smem, p.stream>>>(a, m, scratch); PTG_CHECK_LAUNCH(); ++p.launches; }
+    if constexpr (OP != OP_SIMULATE) {
+        if (which & 4) { mp_rows_inv<T, M, OP><<<grid, NT, smem, p.stream>>>(a, m, scratch); PTG_CHECK_LAUNCH(); ++p.launches; }
+    }
+}
+
+// positions [first, first+count) through the three passes, in scratch-sized sub-chunks
+template <typename T, int OP>
+void launch_mp(Plan& p, const FrameArgs<T>& a, int first, int count, int which = 7) {
+    for (int s = 0; s < count; s += p.mp_chunk) {
+        const int cnt = std::min(p.mp_chunk, count - s);
+        switch (p.M) {
+            case 128: launch_mp_t<T, 128, OP>(p, a, first + s, cnt, which); break;
+            case 256: launch_mp_t<T, 256, OP>(p, a, first + s, cnt, which); break;
+            case 512: launch_mp_t<T, 512, OP>(p, a, first + s, cnt, which); break;
+            default: raise(PTG_ERR_INTERNAL, "multi-pass frame size");
+        }
+    }
 }
 
 template <typename T>
@@ -562,7 +602,14 @@ void build_chunks(Plan& p) {
         p.chunks.push_back(std::move(c));
     }
     p.stash.alloc(std::max<size_t>(1, (size_t)cs * p.w * p.w) * p.celem());
-    p.misfit.alloc(std::max<size_t>(1, (size_t)p.N) * sizeof(double));
+    p.mp = !frame_single_cta(p.prec, p.M);
+    p.misfit_per_pos = p.mp ? p.M / kMpLines : 1;
+    if (p.mp) {   // ~64 MiB of whole-frame scratch: stays L2-resident between passes
+        const size_t fb = p.MM() * p.celem();
+        p.mp_chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(p.N, 1), ((size_t)64 << 20) / fb));
+        p.mp_scratch.alloc((size_t)p.mp_chunk * fb);
+    }
+    p.misfit.alloc(std::max<size_t>(1, (size_t)p.N * p.misfit_per_pos) * sizeof(double));
     // dot partials: one per tile (single chunk) or one per k_shift block
     p.dotp.alloc(std::max<size_t>((size_t)ntiles, 1024) * sizeof(double));
 }
@@ -723,10 +770,15 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
             // frame_kernel writes stash[j*w*w]; offset the base so j - first maps to 0
             a.stash = reinterpret_cast<C*>(p.stash.as<C>()) - (size_t)c.first * p.w * p.w;
             p.ev_begin(0);
-            if (metric == PTG_DISTANCE) launch_objective<T, OP_DISTANCE>(p, a, c.count, z, data);
-            else launch_objective<T, OP_INTENSITY>(p, a, c.count, z, data);
+            if (p.mp) {
+                if (metric == PTG_DISTANCE) launch_mp<T, OP_DISTANCE>(p, a, c.first, c.count);
+                else launch_mp<T, OP_INTENSITY>(p, a, c.first, c.count);
+            } else {
+                if (metric == PTG_DISTANCE) launch_objective<T, OP_DISTANCE>(p, a, c.count, z, data);
+                else launch_objective<T, OP_INTENSITY>(p, a, c.count, z, data);
+                ++p.launches;
+            }
             p.ev_end();
-            ++p.launches;
         }
         if (c.ntiles > 0) {
             // single-chunk plans fuse the shift, <v,z> and the final value reduction
@@ -748,7 +800,7 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
                 c.tile_list.as<const int4>(), p.n, p.w, p.tiles_x,
                 single ? static_cast<const C*>(v) : (const C*)nullptr, static_cast<const C*>(z),
                 static_cast<C*>(grad), p.dotp.as<double>(), single ? 0 : 1, p.misfit.as<const double>(),
-                p.N, single ? value_dev : (double*)nullptr, p.counter.as<unsigned int>()));
+                p.N * p.misfit_per_pos, single ? value_dev : (double*)nullptr, p.counter.as<unsigned int>()));
             p.ev_end();
             ++p.launches;
         }
@@ -763,8 +815,8 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
         ++p.launches;
         ndot = blocks;
     }
-    k_finalize<<<1, 256, 0, p.stream>>>(p.misfit.as<const double>(), p.N, p.dotp.as<const double>(), ndot,
-                                        value_dev);
+    k_finalize<<<1, 256, 0, p.stream>>>(p.misfit.as<const double>(), p.N * p.misfit_per_pos,
+                                        p.dotp.as<const double>(), ndot, value_dev);
     PTG_CHECK_LAUNCH();
     ++p.launches;
 }
@@ -789,8 +841,12 @@ static void simulate_t(Plan& p, const void* z) {
     for (auto& c : p.chunks) {
         if (c->count <= 0) continue;
         a.first = c->first;
-        launch_frame_m<T, OP_SIMULATE>(p.M, a, c->count, p.stream);
-        ++p.launches;
+        if (p.mp) {
+            launch_mp<T, OP_SIMULATE>(p, a, c->first, c->count, 3);
+        } else {
+            launch_frame_m<T, OP_SIMULATE>(p.M, a, c->count, p.stream);
+            ++p.launches;
+        }
     }
 }
 
@@ -820,8 +876,12 @@ static void project_t(Plan& p, const void* z, int k, void* out) {
     p.frame.ensure(p.MM() * p.celem() * 2);
     a.first = k;
     a.frame_out = p.frame.as<cplx<T>>() - (size_t)k * p.MM();
-    launch_frame_m<T, OP_PROJECT>(p.M, a, 1, p.stream);
-    ++p.launches;
+    if (p.mp) {
+        launch_mp<T, OP_PROJECT>(p, a, k, 1);
+    } else {
+        launch_frame_m<T, OP_PROJECT>(p.M, a, 1, p.stream);
+        ++p.launches;
+    }
     // ref mode: return the projection in object coordinates (objectives.cpp:42-50)
     const int r0 = p.ref_mode() ? p.pos_h[2 * k] : 0, c0 = p.ref_mode() ? p.pos_h[2 * k + 1] : 0;
     k_roll<T><<<grid_for(p.MM()), 256, 0, p.stream>>>(p.frame.as<const cplx<T>>(), p.M, r0, c0,
@@ -839,6 +899,37 @@ void plan_project(Plan& p, const void* z, int k, void* out) {
 }
 
 // -------------------------------------------------------------------- PIE
+// z_win += weight o (Pi(psi) - psi) for one position (multi-pass frames)
+template <typename T>
+__global__ void k_pie_update(cplx<T>* __restrict__ z, const cplx<T>* __restrict__ proj,
+                             const cplx<T>* __restrict__ probe, int r0, int c0, int n, int w, int M,
+                             const cplx<T>* __restrict__ wgt, T damping) {
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < w * w; idx += gridDim.x * blockDim.x) {
+        const int r = idx / w, c = idx % w;
+        cplx<T>* zp = z + (size_t)(r0 + r) * n + (c0 + c);
+        const cplx<T> zz = *zp;
+        const cplx<T> psi = probe ? cmul(probe[(size_t)r * M + c], zz) : zz;
+        const cplx<T> dl = csub(proj[(size_t)r * M + c], psi);
+        *zp = cadd(zz, wgt ? cmul(wgt[idx], dl) : cscale(dl, damping));
+    }
+}
+
+template <typename T>
+static void pie_sweep_mp(Plan& p, void* z, const void* wgt, double damping) {
+    p.frame.ensure(p.MM() * p.celem() * 2 + (size_t)p.w * p.w * p.celem());
+    FrameArgs<T> a = frame_args<T>(p, z, p.amp.as<const T>());
+    for (int k = 0; k < p.N; ++k) {
+        a.first = k;
+        a.frame_out = p.frame.as<cplx<T>>() - (size_t)k * p.MM();
+        launch_mp<T, OP_PROJECT>(p, a, k, 1);
+        k_pie_update<T><<<grid_for((size_t)p.w * p.w), 256, 0, p.stream>>>(
+            static_cast<cplx<T>*>(z), p.frame.as<const cplx<T>>(), p.has_probe ? p.probe.as<const cplx<T>>() : nullptr,
+            p.pos_h[2 * k], p.pos_h[2 * k + 1], p.n, p.w, p.M, static_cast<const cplx<T>*>(wgt), (T)damping);
+        PTG_CHECK_LAUNCH();
+        ++p.launches;
+    }
+}
+
 void plan_pie_sweep(Plan& p, void* z, double gamma) {
     LaunchScope ls(p);
     if (gamma < 0.0) raise(PTG_ERR_CONFIG, "pie: gamma must be non-negative");
@@ -867,6 +958,11 @@ void plan_pie_sweep(Plan& p, void* z, double gamma) {
         wgt = dw;
     }
     const double damping = 1.0 / (1.0 + gamma);
+    if (p.mp) {   // frames beyond one CTA: per position, project (3 passes) then update
+        if (p.prec == PTG_C64) pie_sweep_mp<float>(p, z, wgt, damping);
+        else pie_sweep_mp<double>(p, z, wgt, damping);
+        return;
+    }
     if (p.prec == PTG_C64) launch_pie<float>(p, z, wgt, damping);
     else launch_pie<double>(p, z, wgt, damping);
 }

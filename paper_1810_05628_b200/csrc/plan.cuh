@@ -101,6 +101,12 @@ struct Plan {
     std::vector<TmEntry> tm_z_cache = std::vector<TmEntry>(8);
     size_t tm_z_next = 0;
 
+    // multi-pass path for frames larger than one CTA (frame_multipass.cuh)
+    bool mp = false;
+    int mp_chunk = 0;                // positions per scratch sub-chunk
+    DevMem mp_scratch;               // mp_chunk x M x M complex
+    int misfit_per_pos = 1;          // partial objective values per position
+
     int tiles_x = 0, tiles_y = 0;
     int chunk_size = 0;
     std::vector<std::unique_ptr<Chunk>> chunks;
