@@ -202,9 +202,10 @@ int ptg_plan_get_timing(ptg_plan* plan, double* frame_ms, int64_t* frame_launche
                         double* gather_ms, int64_t* gather_launches) {
     return guard([&] {
         ptg::Plan& p = P(plan);
-        double ms[2];
-        int64_t cnt[2];
+        double ms[3];
+        int64_t cnt[3];
         p.timing_collect(ms, cnt);
+        if (cnt[2]) fprintf(stderr, "[ptg] probe launches: %lld, avg %.3f us\n", (long long)cnt[2], 1e3 * ms[2] / cnt[2]);
         if (frame_ms) *frame_ms = ms[0];
         if (frame_launches) *frame_launches = cnt[0];
         if (gather_ms) *gather_ms = ms[1];

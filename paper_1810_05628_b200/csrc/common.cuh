@@ -112,6 +112,12 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
 }
 #endif
 
+// Per-position contribution ("stash") rows have pitch >= w + 2, rounded up to
+// even: the window row is stored at offset (col0 & 1) with zeros elsewhere, so
+// every even-aligned pixel pair of the object maps to one aligned 16-byte
+// (complex64) vector of the stash (plan.cu k_overlap_gather).
+__host__ __device__ constexpr int stash_pitch(int w) { return (w + 3) & ~1; }
+
 inline int ilog2(int n) { int l = 0; while ((1 << l) < n) ++l; return l; }
 inline bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 

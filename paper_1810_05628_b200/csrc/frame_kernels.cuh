@@ -33,6 +33,10 @@ struct FrameArgs {
     T* data_out;             // OP_SIMULATE: N x M x M intensities
     double* misfit;          // per-pattern objective contribution
     int n, w, first;         // pattern index = first + blockIdx.x
+    // colour-plane overlap-add (plan.cuh): contribution of pattern j goes to
+    // planes[color[j]] at its window (nullptr = stash mode)
+    cplx<T>* planes;
+    const int* color;
 };
 
 // Deterministic block reduction (fixed shuffle tree + fixed warp order).
@@ -136,11 +140,25 @@ __global__ void __launch_bounds__(NT) frame_kernel(FrameArgs<T> a) {
             //   distance : conj(P) (psi - Pi(psi)) = conj(P) ifft2(R)           (x 1/M^2)
             //   intensity: 2 M^2 conj(P) ifft2(r W) = 2 conj(P) IDFT_unnorm(R)  (objectives.cpp:98-102)
             const T sc = (OP == OP_DISTANCE) ? T(1) / (T(M) * T(M)) : T(2);
-            C* out = a.stash + (size_t)j * w * w;
-            for (int idx = threadIdx.x; idx < w * w; idx += NT) {
-                const int r = idx / w, c = idx % w;
-                C v = cscale(buf[r * S + c], sc);
-                if (a.probe) v = cmulc(a.probe[r * M + c], v);
+            if (a.planes) {   // colour plane: plain stores into the window
+                C* pl = a.planes + (size_t)a.color[j] * n * n + (size_t)p.x * n + p.y;
+                for (int idx = threadIdx.x; idx < w * w; idx += NT) {
+                    const int r = idx / w, c = idx % w;
+                    C v = cscale(buf[r * S + c], sc);
+                    if (a.probe) v = cmulc(a.probe[r * M + c], v);
+                    pl[(size_t)r * n + c] = v;
+                }
+                return;
+            }
+            const int sp = stash_pitch(w), odd = p.y & 1;   // stash row pitch / parity shift
+            C* out = a.stash + (size_t)j * w * sp;
+            for (int idx = threadIdx.x; idx < w * sp; idx += NT) {
+                const int r = idx / sp, e = idx % sp, c = e - odd;
+                C v = mk<T>(T(0), T(0));
+                if ((unsigned)c < (unsigned)w) {
+                    v = cscale(buf[r * S + c], sc);
+                    if (a.probe) v = cmulc(a.probe[r * M + c], v);
+                }
                 out[idx] = v;
             }
         }

@@ -148,15 +148,17 @@ __global__ void __launch_bounds__(mp_threads<M>()) mp_rows_inv(FrameArgs<T> a, M
         for (int idx = threadIdx.x; idx < NL * M; idx += NT) out[idx] = cscale(buf[(idx / M) * S + idx % M], inv);
     } else {
         const T sc = (OP == OP_DISTANCE) ? inv : T(2);
-        const int w = a.w;
-        C* out = a.stash + (size_t)j * w * w;
-        for (int idx = threadIdx.x; idx < NL * M; idx += NT) {
-            const int rl = idx / M, c = idx % M, r = r0 + rl;
-            if (r < w && c < w) {
-                C v = cscale(buf[rl * S + c], sc);
+        const int w = a.w, sp = stash_pitch(w), odd = a.pos[j].y & 1;   // stash pitch / parity shift
+        C* out = a.stash + (size_t)j * w * sp;
+        for (int idx = threadIdx.x; idx < NL * sp; idx += NT) {
+            const int rl = idx / sp, e = idx % sp, r = r0 + rl, c = e - odd;
+            if (r >= w) continue;
+            C v = mk<T>(T(0), T(0));
+            if ((unsigned)c < (unsigned)w) {
+                v = cscale(buf[rl * S + c], sc);
                 if (a.probe) v = cmulc(a.probe[(size_t)r * M + c], v);
-                out[(size_t)r * w + c] = v;
             }
+            out[(size_t)r * sp + e] = v;
         }
     }
 }

@@ -222,15 +222,29 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // epilogue: contribution = sc * conj(P) o IDFT_u(R) = sc * conj(P o conj(x))
     if (live) {
+        // stash row pitch M + 2, window row at offset (col0 & 1), zero pads (plan.cuh)
         const float sc = (OP == OP_DISTANCE) ? 1.f / (float(M) * float(M)) : 2.f;
-        float2* __restrict__ out = a.stash + (size_t)j * M * M + t;
         if constexpr (PROBE) mbar_wait(&bar_p[f], 0);
+        if (a.planes) {   // colour plane: plain coalesced stores into the window
+            float2* __restrict__ pl = a.planes + (size_t)a.color[j] * a.n * a.n + (size_t)pj.x * a.n + pj.y + t;
+#pragma unroll
+            for (int r = 0; r < M; ++r) {
+                float2 v = make_float2(x[r].x * sc, -x[r].y * sc);
+                if constexpr (PROBE) v = cmulc(buf[r * M + t], v);
+                pl[(size_t)r * a.n] = v;
+            }
+            return;
+        }
+        float2* __restrict__ out = a.stash + (size_t)j * M * S;
 #pragma unroll
         for (int r = 0; r < M; ++r) {
             float2 v = make_float2(x[r].x * sc, -x[r].y * sc);   // sc * IDFT_u(R)
             if constexpr (PROBE) v = cmulc(buf[r * M + t], v);   // probe tile (dense pitch M)
-            out[(size_t)r * M] = v;
+            out[(size_t)r * S + odd + t] = v;
         }
+        // the two zero pads of row t
+        out[(size_t)t * S + (odd ? 0 : M)] = make_float2(0.f, 0.f);
+        out[(size_t)t * S + M + 1] = make_float2(0.f, 0.f);
     }
 }
 

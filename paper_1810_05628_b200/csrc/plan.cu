@@ -50,9 +50,9 @@ void Plan::ev_end() {
     ++ev_used;
 }
 
-void Plan::timing_collect(double* ms, int64_t* cnt) {
-    ms[0] = ms[1] = 0.0;
-    cnt[0] = cnt[1] = 0;
+void Plan::timing_collect(double* ms, int64_t* cnt) {   // ms[3], cnt[3] (kind 2 = probes)
+    ms[0] = ms[1] = ms[2] = 0.0;
+    cnt[0] = cnt[1] = cnt[2] = 0;
     for (size_t i = 0; i < ev_used; ++i) {
         PTG_CUDA(cudaEventSynchronize(ev_pool[i].b));
         float t = 0.f;
@@ -67,7 +67,7 @@ size_t Plan::device_bytes() const {
     size_t b = pos.bytes + probe.bytes + amp.bytes + inten.bytes + stash.bytes + misfit.bytes +
                dotp.bytes + value.bytes + scratch.bytes + flag.bytes + frame.bytes + zbuf.bytes +
                vbuf.bytes + gbuf.bytes + stage.bytes;
-    for (const auto& c : chunks) b += c->tile_ids.bytes + c->tile_ptr.bytes + c->tile_list.bytes;
+    for (const auto& c : chunks) b += c->tile_ids.bytes + c->tile_list.bytes;
     return b;
 }
 
@@ -270,6 +270,8 @@ FrameArgs<T> frame_args(Plan& p, const void* z, const T* amp) {
     a.amp = amp;
     a.stash = p.stash.as<cplx<T>>();
     a.misfit = p.misfit.as<double>();
+    a.planes = p.planes_mode ? p.planes.as<cplx<T>>() : nullptr;
+    a.color = p.planes_mode ? p.color.as<const int>() : nullptr;
     a.n = p.n;
     a.w = p.w;
     return a;
@@ -281,8 +283,22 @@ __device__ __forceinline__ void finalize_block(const double* misfit, int N, cons
                                                double* out, double* red, int lin) {
     double m = 0.0, d = 0.0;
     const int cm = (N + 255) / 256, cd = (ndot + 255) / 256;
-    for (int i = lin * cm, e = min(i + cm, N); i < e; ++i) m += __ldcg(misfit + i);
-    for (int i = lin * cd, e = min(i + cd, ndot); i < e; ++i) d += __ldcg(dotp + i);
+    // loads batched ahead of the (in-order) sums: one L2 round trip per 8 values
+    constexpr int B = 8;
+    for (int i = lin * cm, e = min(i + cm, N); i < e; i += B) {
+        double t[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) t[u] = i + u < e ? __ldcg(misfit + i + u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < B; ++u) m += t[u];
+    }
+    for (int i = lin * cd, e = min(i + cd, ndot); i < e; i += B) {
+        double t[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) t[u] = i + u < e ? __ldcg(dotp + i + u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < B; ++u) d += t[u];
+    }
     double both[2] = {m, d};
     double res[2];
 #pragma unroll
@@ -301,76 +317,176 @@ __device__ __forceinline__ void finalize_block(const double* misfit, int N, cons
     if (lin == 0) *out = res[0] - res[1];
 }
 
+// ------------------------------------------------------ colour-plane reduce
+constexpr int kPlaneBlocks = 148 * 4;   // fixed grid => fixed dot partition (deterministic)
+// grad = sum_c planes[c] (fixed colour order) - v, <v,z> partials, fused final
+// value (last block).  Pure streaming: every thread owns a fixed pixel pair.
+template <typename T>
+__global__ void __launch_bounds__(256) k_plane_reduce(const cplx<T>* __restrict__ planes, int ncol, size_t nn,
+                                                      const cplx<T>* __restrict__ v, const cplx<T>* __restrict__ z,
+                                                      cplx<T>* __restrict__ grad, double* __restrict__ dotp,
+                                                      const double* __restrict__ misfit, int N,
+                                                      double* value_out, unsigned int* counter) {
+    __shared__ double red[8];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int lin = threadIdx.x;
+    const size_t npairs = (nn + 1) / 2;
+    const size_t chunk = (npairs + gridDim.x - 1) / gridDim.x;
+    const size_t lo = blockIdx.x * chunk, hi = min(lo + chunk, npairs);
+    double d = 0.0;
+    for (size_t pr = lo + lin; pr < hi; pr += blockDim.x) {
+        const size_t i = 2 * pr;
+        const bool two = i + 1 < nn;
+        cplx<T> a0 = mk<T>(T(0), T(0)), a1 = a0;
+        constexpr int B = 8;
+        for (int c0 = 0; c0 < ncol; c0 += B) {
+            cplx<T> q0[B], q1[B];
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                q0[u] = q1[u] = mk<T>(T(0), T(0));
+                if (c0 + u < ncol) {
+                    const cplx<T>* s = planes + (size_t)(c0 + u) * nn + i;
+                    if constexpr (sizeof(T) == 4) {
+                        if (two && (nn % 2 == 0)) {   // 16-B aligned pair
+                            const float4 f = __ldg(reinterpret_cast<const float4*>(s));
+                            q0[u] = mk<T>(f.x, f.y);
+                            q1[u] = mk<T>(f.z, f.w);
+                        } else {
+                            q0[u] = s[0];
+                            if (two) q1[u] = s[1];
+                        }
+                    } else {
+                        q0[u] = s[0];
+                        if (two) q1[u] = s[1];
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                a0 = cadd(a0, q0[u]);
+                a1 = cadd(a1, q1[u]);
+            }
+        }
+        if (v) {
+            const cplx<T> v0 = v[i], z0 = z[i];
+            a0 = csub(a0, v0);
+            d += (double)v0.x * (double)z0.x + (double)v0.y * (double)z0.y;
+            if (two) {
+                const cplx<T> v1 = v[i + 1], z1 = z[i + 1];
+                a1 = csub(a1, v1);
+                d += (double)v1.x * (double)z1.x + (double)v1.y * (double)z1.y;
+            }
+        }
+        grad[i] = a0;
+        if (two) grad[i + 1] = a1;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if ((lin & 31) == 0) red[lin >> 5] = d;
+    __syncthreads();
+    if (lin == 0) {
+        double s = 0.0;
+        for (int k = 0; k < 8; ++k) s += red[k];
+        dotp[blockIdx.x] = s;
+    }
+    __shared__ bool last;
+    if (lin == 0) {
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        finalize_block(misfit, N, dotp, gridDim.x, value_out, red, lin);
+        if (lin == 0) *counter = 0u;
+    }
+}
+
 // --------------------------------------------------------- overlap gather
 template <typename T>
 __global__ void __launch_bounds__(256) k_overlap_gather(
     const cplx<T>* __restrict__ stash, const int* __restrict__ tile_ids,
-    const int* __restrict__ tile_ptr, const int4* __restrict__ entries, int n, int w, int tiles_x,
+    int cap, const int4* __restrict__ entries, int n, int w, int tiles_x,
     const cplx<T>* __restrict__ v,
     const cplx<T>* __restrict__ z, cplx<T>* __restrict__ grad, double* __restrict__ dotp,
     int accumulate, const double* __restrict__ misfit, int N, double* value_out,
     unsigned int* counter) {
     __shared__ double red[8];
-    constexpr int PPT = kTileH / 8;   // pixels (rows) per thread
     // programmatic dependent launch: everything above overlaps the frame
     // kernel's tail; wait here until its stash/misfit writes are visible
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int t = tile_ids ? tile_ids[blockIdx.x] : blockIdx.x;
     const int ty = t / tiles_x, tx = t % tiles_x;
-    const int x = tx * kTileW + threadIdx.x;
-    const int y0 = ty * kTileH + threadIdx.y;
-    const int lin = threadIdx.y * kTileW + threadIdx.x;
-    // PPT pixels per thread (rows y0 + 8i).  The tile's windows (ascending scan
-    // order, host-precomputed as {stash offset - r0*w - c0, r0, c0}) are read
-    // with warp-uniform 16-B loads; per pixel an add, a compare and a
-    // predicated stash load; U entries in flight; adds strictly in list order
-    // (the reference's accumulation order)
-    constexpr int U = 8;
-    cplx<T> acc[PPT];
-    int pix[PPT];
-#pragma unroll
-    for (int i = 0; i < PPT; ++i) {
-        acc[i] = mk<T>(T(0), T(0));
-        pix[i] = (y0 + 8 * i) * w + x;
+    const int x = tx * kTileW + 2 * threadIdx.x;   // this lane's pixel pair (x, x+1), x even
+    const int y = ty * kTileH + threadIdx.y;
+    const int lin = threadIdx.y * 32 + threadIdx.x;
+    const int sp = stash_pitch(w);
+    // The tile's windows, in ascending scan order, are host-precomputed at a
+    // fixed stride `cap` (padded with never-matching entries) as
+    // {stash offset - r0*sp - even(c0), r0, even(c0)}.  Thanks to the stash
+    // layout (parity-shifted, zero-padded rows of pitch w+2) a window touching
+    // the pair contributes exactly one aligned 16-byte vector, zeros included:
+    // one uniform entry load + one predicated vector load per window; the
+    // adds follow the list (= the reference's accumulation order).
+    constexpr int U = 16;
+    cplx<T> a0 = mk<T>(T(0), T(0)), a1 = a0, v0 = a0, v1 = a0, z0 = a0, z1 = a0;
+    const bool in0 = x < n && y < n, in1 = x + 1 < n && y < n;
+    if (v) {   // shift operands prefetched off the critical path
+        if (in0) { v0 = v[(size_t)y * n + x]; z0 = z[(size_t)y * n + x]; }
+        if (in1) { v1 = v[(size_t)y * n + x + 1]; z1 = z[(size_t)y * n + x + 1]; }
     }
-    const int e0 = tile_ptr[blockIdx.x], cnt = tile_ptr[blockIdx.x + 1] - e0;
-    const int4* __restrict__ E = entries + e0;
-    for (int e = 0; e < cnt; e += U) {
+    const int pix = y * sp + x;
+    // the block's entry list is staged once in shared memory: a warp-uniform
+    // global LDG.128 would still move 512 B through the L1 data path per warp,
+    // a broadcast LDS.128 costs one wavefront
+    constexpr int LCAP = 256;
+    __shared__ int4 s_e[LCAP];
+    const int4* __restrict__ E = entries + (size_t)blockIdx.x * cap;
+    for (int base = 0; base < cap; base += LCAP) {
+    const int ccap = min(LCAP, cap - base);
+    __syncthreads();
+    for (int i = lin; i < ccap; i += 256) s_e[i] = __ldg(E + base + i);
+    __syncthreads();
+    for (int e = 0; e < ccap; e += U) {
         int4 en[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) en[u] = __ldg(E + min(e + u, cnt - 1));
-        cplx<T> val[U][PPT];
-        bool ok[U][PPT];
+        for (int u = 0; u < U; ++u) en[u] = s_e[e + u];
+        cplx<T> p0[U], p1[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const bool inx = (e + u < cnt) && (unsigned)(x - en[u].z) < (unsigned)w;
-#pragma unroll
-            for (int i = 0; i < PPT; ++i) {
-                ok[u][i] = inx && (unsigned)(y0 + 8 * i - en[u].y) < (unsigned)w;
-                val[u][i] = ok[u][i] ? stash[en[u].x + pix[i]] : mk<T>(T(0), T(0));
+            const bool ok = (unsigned)(x - en[u].z) < (unsigned)(w + 2) && (unsigned)(y - en[u].y) < (unsigned)w;
+            const cplx<T>* s = stash + (ok ? en[u].x + pix : 0);
+            if constexpr (sizeof(T) == 4) {
+                float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (ok) q = __ldg(reinterpret_cast<const float4*>(s));
+                p0[u] = mk<T>(q.x, q.y);
+                p1[u] = mk<T>(q.z, q.w);
+            } else {
+                p0[u] = ok ? s[0] : mk<T>(T(0), T(0));
+                p1[u] = ok ? s[1] : mk<T>(T(0), T(0));
             }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-            for (int i = 0; i < PPT; ++i)
-                if (ok[u][i]) acc[i] = cadd(acc[i], val[u][i]);
+        for (int u = 0; u < U; ++u) {
+            a0 = cadd(a0, p0[u]);
+            a1 = cadd(a1, p1[u]);
+        }
+    }
     }
     double d = 0.0;
+    cplx<T> g[2] = {a0, a1};
+    const cplx<T> vv[2] = {v0, v1}, zz[2] = {z0, z1};
+    const bool in[2] = {in0, in1};
 #pragma unroll
-    for (int i = 0; i < PPT; ++i) {
-        const int y = y0 + 8 * i;
-        if (x < n && y < n) {
-            const size_t idx = (size_t)y * n + x;
-            cplx<T> g = acc[i];
-            if (accumulate) g = cadd(grad[idx], g);
-            if (v) {
-                const cplx<T> vv = v[idx], zz = z[idx];
-                g = csub(g, vv);
-                d += (double)vv.x * (double)zz.x + (double)vv.y * (double)zz.y;
-            }
-            grad[idx] = g;
+    for (int i = 0; i < 2; ++i) {
+        if (!in[i]) continue;
+        const size_t idx = (size_t)y * n + x + i;
+        if (accumulate) g[i] = cadd(grad[idx], g[i]);
+        if (v) {
+            g[i] = csub(g[i], vv[i]);
+            d += (double)vv[i].x * (double)zz[i].x + (double)vv[i].y * (double)zz[i].y;
         }
+        grad[idx] = g[i];
     }
     if (v || value_out) {
 #pragma unroll
@@ -552,11 +668,73 @@ void launch_pie(Plan& p, void* z, const void* wgt, double damping) {
     }
 }
 
+// ----------------------------------------------------------- colour planes
+// Greedy colouring of the window-overlap graph in scan order (windows j, k
+// overlap iff |dr| < w and |dc| < w); a raster with stride s gets
+// ceil(w/s)^2 colours.  Deterministic for given positions.
+int colour_positions(const Plan& p, std::vector<int>& color) {
+    const int w = p.w, G = std::max(1, (p.n + w - 1) / w);
+    std::vector<std::vector<int>> cells((size_t)G * G);
+    color.assign(p.N, 0);
+    int ncol = 0;
+    std::vector<char> used;
+    for (int j = 0; j < p.N; ++j) {
+        const int r = p.pos_h[2 * j], c = p.pos_h[2 * j + 1];
+        const int cy = std::min(r / w, G - 1), cx = std::min(c / w, G - 1);
+        used.assign(ncol + 1, 0);
+        for (int yy = std::max(0, cy - 1); yy <= std::min(G - 1, cy + 1); ++yy)
+            for (int xx = std::max(0, cx - 1); xx <= std::min(G - 1, cx + 1); ++xx)
+                for (int k : cells[(size_t)yy * G + xx])
+                    if (std::abs(p.pos_h[2 * k] - r) < w && std::abs(p.pos_h[2 * k + 1] - c) < w) used[color[k]] = 1;
+        int col = 0;
+        while (used[col]) ++col;
+        color[j] = col;
+        ncol = std::max(ncol, col + 1);
+        cells[(size_t)cy * G + cx].push_back(j);
+    }
+    return ncol;
+}
+
+// Planes when they stream no more than ~2x the stash's bytes and stay small:
+// a plain streaming reduction beats the list-driven gather by far.
+bool choose_planes(Plan& p) {
+    if (p.N == 0 || p.mp) return false;
+    static const bool off = getenv("PTG_NO_PLANES") && getenv("PTG_NO_PLANES")[0] == '1';   // A/B switch
+    if (off) return false;
+    std::vector<int> color;
+    const int ncol = colour_positions(p, color);
+    const double plane_elems = (double)ncol * p.nn();
+    const double stash_elems = (double)p.N * p.w * stash_pitch(p.w);
+    if (plane_elems > 2.0 * stash_elems || plane_elems * p.celem() > (double)(512u << 20)) return false;
+    p.ncolors = ncol;
+    p.color_h = color;
+    p.color.alloc(color.size() * sizeof(int));
+    PTG_CUDA(cudaMemcpy(p.color.p, color.data(), color.size() * sizeof(int), cudaMemcpyHostToDevice));
+    p.planes.alloc((size_t)ncol * p.nn() * p.celem());
+    PTG_CUDA(cudaMemset(p.planes.p, 0, p.planes.bytes));   // untouched pixels stay zero forever
+    return true;
+}
+
 // --------------------------------------------------------- chunks / tiles
 void build_chunks(Plan& p) {
     p.tiles_x = (p.n + kTileW - 1) / kTileW;
     p.tiles_y = (p.n + kTileH - 1) / kTileH;
-    const size_t per = (size_t)p.w * p.w * p.celem();
+    p.mp = !frame_single_cta(p.prec, p.M);
+    p.planes_mode = choose_planes(p);
+    if (p.planes_mode) {   // one chunk, no tile lists, no stash
+        auto c = std::make_unique<Chunk>();
+        c->first = 0;
+        c->count = p.N;
+        p.chunk_size = p.N;
+        p.chunks.clear();
+        p.chunks.push_back(std::move(c));
+        p.stash.alloc(p.celem());
+        p.misfit_per_pos = 1;
+        p.misfit.alloc(std::max<size_t>(1, (size_t)p.N) * sizeof(double));
+        p.dotp.alloc((size_t)kPlaneBlocks * sizeof(double));
+        return;
+    }
+    const size_t per = (size_t)p.w * stash_pitch(p.w) * p.celem();
     const size_t budget = (size_t)2 << 30;   // stash bytes per chunk
     int cs = p.N > 0 ? (int)std::min<size_t>((size_t)p.N, std::max<size_t>(1, budget / per)) : 1;
     p.chunk_size = cs;
@@ -572,37 +750,46 @@ void build_chunks(Plan& p) {
         for (int j = c->first; j < c->first + c->count; ++j) {
             const int r0 = p.pos_h[2 * j], c0 = p.pos_h[2 * j + 1];
             const int ty0 = r0 / kTileH, ty1 = (r0 + p.w - 1) / kTileH;
-            const int tx0 = c0 / kTileW, tx1 = (c0 + p.w - 1) / kTileW;
+            // pixel pairs (even x) touching [c0, c0 + w): x in [c0 - (c0 & 1), c0 + w)
+            const int tx0 = (c0 - (c0 & 1)) / kTileW, tx1 = (c0 + p.w - 1) / kTileW;
             for (int ty = ty0; ty <= ty1; ++ty)
                 for (int tx = tx0; tx <= tx1; ++tx) lists[ty * p.tiles_x + tx].push_back(j);
         }
-        std::vector<int> ids, ptr{0};
-        std::vector<int4> list;   // {stash offset of window origin - r0*w - c0, r0, c0, j}
+        std::vector<int> ids;
+        // Per visited tile, a fixed-stride (cap) list of the windows covering it in
+        // ascending scan order: {stash offset of window origin - r0*w - c0, r0, c0, j},
+        // padded with entries that never match (so no per-tile count is needed).
         c->all_tiles = (nchunks == 1);
+        size_t cap = 1;
         for (int t = 0; t < ntiles; ++t) {
             if (!c->all_tiles && lists[t].empty()) continue;
             ids.push_back(t);
-            for (int j : lists[t]) {
-                const int r0 = p.pos_h[2 * j], c0 = p.pos_h[2 * j + 1];
-                const long long off = (long long)(j - c->first) * p.w * p.w - (long long)r0 * p.w - c0;
-                list.push_back(make_int4((int)off, r0, c0, j));
-            }
-            ptr.push_back((int)list.size());
+            cap = std::max(cap, lists[t].size());
         }
+        cap = (cap + 15) / 16 * 16;   // multiple of the gather's batch U
+        const int4 pad = make_int4(0, -(1 << 29), -(1 << 29), -1);
+        std::vector<int4> list(ids.size() * cap, pad);
+        for (size_t b = 0; b < ids.size(); ++b) {
+            size_t e = 0;
+            for (int j : lists[ids[b]]) {
+                const int r0 = p.pos_h[2 * j], c0 = p.pos_h[2 * j + 1];
+                const int sp = stash_pitch(p.w), c0e = c0 - (c0 & 1);
+                const long long off = (long long)(j - c->first) * p.w * sp - (long long)r0 * sp - c0e;
+                list[b * cap + e++] = make_int4((int)off, r0, c0e, j);
+            }
+        }
+        c->cap = (int)cap;
         c->ntiles = (int)ids.size();
         if (!c->all_tiles) {
             c->tile_ids.alloc(ids.size() * sizeof(int));
             if (!ids.empty()) PTG_CUDA(cudaMemcpy(c->tile_ids.p, ids.data(), ids.size() * sizeof(int), cudaMemcpyHostToDevice));
         }
-        c->tile_ptr.alloc(ptr.size() * sizeof(int));
-        PTG_CUDA(cudaMemcpy(c->tile_ptr.p, ptr.data(), ptr.size() * sizeof(int), cudaMemcpyHostToDevice));
         // int32 stash offsets: the per-chunk stash budget keeps them < 2^31 elements
         c->tile_list.alloc(std::max<size_t>(1, list.size()) * sizeof(int4));
         if (!list.empty()) PTG_CUDA(cudaMemcpy(c->tile_list.p, list.data(), list.size() * sizeof(int4), cudaMemcpyHostToDevice));
         p.chunks.push_back(std::move(c));
     }
-    p.stash.alloc(std::max<size_t>(1, (size_t)cs * p.w * p.w) * p.celem());
-    p.mp = !frame_single_cta(p.prec, p.M);
+    p.stash.alloc(std::max<size_t>(1, (size_t)cs * p.w * stash_pitch(p.w)) * p.celem());
     p.misfit_per_pos = p.mp ? p.M / kMpLines : 1;
     if (p.mp) {   // ~64 MiB of whole-frame scratch: stays L2-resident between passes
         const size_t fb = p.MM() * p.celem();
@@ -761,6 +948,10 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
     using C = cplx<T>;
     const T* data = metric == PTG_DISTANCE ? p.amp.as<const T>() : p.inten.as<const T>();
     const bool single = p.chunks.size() == 1;
+    // fused last-block finalize in the gather (single-chunk plans); PTG_NOFUSE=1
+    // selects the separate finalize kernel (kept for A/B measurement)
+    static const bool nofuse = getenv("PTG_NOFUSE") && getenv("PTG_NOFUSE")[0] == '1';
+    const bool fuse = single && p.chunks[0]->ntiles > 0 && !nofuse;
     if (!single) dev_fill_zero(p.prec, grad, p.nn(), p.stream);
     for (auto& cp : p.chunks) {
         Chunk& c = *cp;
@@ -768,7 +959,7 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
             FrameArgs<T> a = frame_args<T>(p, z, data);
             a.first = c.first;
             // frame_kernel writes stash[j*w*w]; offset the base so j - first maps to 0
-            a.stash = reinterpret_cast<C*>(p.stash.as<C>()) - (size_t)c.first * p.w * p.w;
+            a.stash = reinterpret_cast<C*>(p.stash.as<C>()) - (size_t)c.first * p.w * stash_pitch(p.w);
             p.ev_begin(0);
             if (p.mp) {
                 if (metric == PTG_DISTANCE) launch_mp<T, OP_DISTANCE>(p, a, c.first, c.count);
@@ -780,33 +971,57 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
             }
             p.ev_end();
         }
+        if (p.planes_mode) {
+            // streaming colour-plane reduction + shift + <v,z> + final value,
+            // chained to the frame kernel by programmatic dependent launch
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(kPlaneBlocks);
+            cfg.blockDim = dim3(256);
+            cfg.stream = p.stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = p.timing ? 0 : 1;
+            p.ev_begin(1);
+            PTG_CUDA(cudaLaunchKernelEx(&cfg, k_plane_reduce<T>, p.planes.as<const C>(), p.ncolors, p.nn(),
+                                        static_cast<const C*>(v), static_cast<const C*>(z), static_cast<C*>(grad),
+                                        p.dotp.as<double>(), p.misfit.as<const double>(), p.N, value_dev,
+                                        p.counter.as<unsigned int>()));
+            p.ev_end();
+            ++p.launches;
+            return;
+        }
         if (c.ntiles > 0) {
             // single-chunk plans fuse the shift, <v,z> and the final value reduction
             // into the gather (last-block-done); it is chained to the frame kernel
             // by programmatic dependent launch so its launch overlaps the frame tail
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(c.ntiles);
-            cfg.blockDim = dim3(kTileW, 8);
+            cfg.blockDim = dim3(kTileW / 2, kTileH);
             cfg.stream = p.stream;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
             attr[0].val.programmaticStreamSerializationAllowed = 1;
             cfg.attrs = attr;
             cfg.numAttrs = p.timing ? 0 : 1;   // event timing needs plain kernel boundaries
-            p.ev_begin(1);
+            static const int reps = getenv("PTG_GATHER_REPS") ? atoi(getenv("PTG_GATHER_REPS")) : 1;   // A/B probe
+            for (int rep = 0; rep < reps; ++rep) {
+            p.ev_begin(rep == 0 ? 1 : 2);
             PTG_CUDA(cudaLaunchKernelEx(
                 &cfg, k_overlap_gather<T>, p.stash.as<const C>(),
-                c.all_tiles ? (const int*)nullptr : c.tile_ids.as<const int>(), c.tile_ptr.as<const int>(),
+                c.all_tiles ? (const int*)nullptr : c.tile_ids.as<const int>(), c.cap,
                 c.tile_list.as<const int4>(), p.n, p.w, p.tiles_x,
                 single ? static_cast<const C*>(v) : (const C*)nullptr, static_cast<const C*>(z),
                 static_cast<C*>(grad), p.dotp.as<double>(), single ? 0 : 1, p.misfit.as<const double>(),
-                p.N * p.misfit_per_pos, single ? value_dev : (double*)nullptr, p.counter.as<unsigned int>()));
+                p.N * p.misfit_per_pos, fuse ? value_dev : (double*)nullptr, p.counter.as<unsigned int>()));
             p.ev_end();
             ++p.launches;
+            }
         }
     }
-    if (single && p.chunks[0]->ntiles > 0) return;   // value produced by the fused gather
-    int ndot = 0;
+    if (fuse) return;   // value produced by the fused gather
+    int ndot = (single && v) ? p.chunks[0]->ntiles : 0;
     if (!single && v) {
         const int blocks = 1024;
         k_shift<T><<<blocks, 256, 0, p.stream>>>(static_cast<const C*>(v), static_cast<const C*>(z),

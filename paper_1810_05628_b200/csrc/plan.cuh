@@ -59,11 +59,12 @@ struct Chunk {
     int first = 0, count = 0;
     int ntiles = 0;          // tiles this chunk's gather visits
     bool all_tiles = false;  // single-chunk plans visit every tile (tile id = block id)
-    DevMem tile_ids, tile_ptr, tile_list;
+    int cap = 0;             // fixed stride of the per-tile window lists
+    DevMem tile_ids, tile_list;
 };
 
-constexpr int kTileW = 32;   // overlap-add gather tile: 32 x 16 pixels, 2 per thread (32 x 8 block)
-constexpr int kTileH = 16;
+constexpr int kTileW = 64;   // overlap-add gather tile: 64 x 8 pixels, 2 per thread (32 x 8 block)
+constexpr int kTileH = 8;
 
 struct Plan {
     int n = 0, M = 0, w = 0, N = 0, prec = PTG_C64, device = 0;
@@ -100,6 +101,16 @@ struct Plan {
     struct TmEntry { const void* ptr = nullptr; alignas(64) unsigned char map[128] = {}; };
     std::vector<TmEntry> tm_z_cache = std::vector<TmEntry>(8);
     size_t tm_z_next = 0;
+
+    // Overlap-add mode.  PLANES: scan positions are coloured into sets of
+    // pairwise non-overlapping windows; each frame stores its contribution
+    // into its colour's n x n plane (plain stores, disjoint within a colour)
+    // and a streaming kernel sums the planes in fixed colour order.  STASH:
+    // per-position contributions + tile-list gather (large problems).
+    bool planes_mode = false;
+    int ncolors = 0;
+    std::vector<int> color_h;
+    DevMem color, planes;
 
     // multi-pass path for frames larger than one CTA (frame_multipass.cuh)
     bool mp = false;
