@@ -57,6 +57,48 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
     return s;
 }
 
+// value = sum_j misfit_j - sum_t dotp_t by NT threads: fixed contiguous
+// partition + fixed shuffle tree + fixed warp order (deterministic).
+// red needs NT / 32 doubles; the result is written by thread 0.
+template <int NT>
+__device__ __forceinline__ void finalize_value(const double* misfit, int N, const double* dotp, int ndot,
+                                               double* out, double* red, int lin) {
+    constexpr int NW = NT / 32;
+    double m = 0.0, d = 0.0;
+    const int cm = (N + NT - 1) / NT, cd = (ndot + NT - 1) / NT;
+    const int m0 = lin * cm, me = min(m0 + cm, N), d0 = lin * cd, de = min(d0 + cd, ndot);
+    // both partitions' loads batched ahead of the (in-order) sums: one L2 round
+    // trip per B values of each
+    constexpr int B = 16;
+    for (int i = 0; i < cm || i < cd; i += B) {
+        double tm[B], td[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) tm[u] = m0 + i + u < me ? __ldcg(misfit + m0 + i + u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < B; ++u) td[u] = d0 + i + u < de ? __ldcg(dotp + d0 + i + u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < B; ++u) m += tm[u];
+#pragma unroll
+        for (int u = 0; u < B; ++u) d += td[u];
+    }
+    double both[2] = {m, d};
+    double res[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        double x = both[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        __syncthreads();
+        if ((lin & 31) == 0) red[lin >> 5] = x;
+        __syncthreads();
+        double s = 0.0;
+        if (lin == 0)
+            for (int i = 0; i < NW; ++i) s += red[i];
+        res[q] = s;
+    }
+    if (lin == 0) *out = res[0] - res[1];
+}
+
 template <typename T, int M>
 __host__ __device__ constexpr size_t frame_smem_bytes(int NT) {
     return sizeof(cplx<T>) * ((size_t)M * frame_stride(M) + M) + sizeof(double) * ((NT + 31) / 32);

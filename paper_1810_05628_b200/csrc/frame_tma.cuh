@@ -148,6 +148,9 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
             // spectral operator on row t; x <- conj(R) feeds the inverse passes
             if (live) {
                 mbar_wait(&bar_a[f], 0);
+                // row misfit: four fp32 partial sums of non-negative terms (short
+                // dependency chains), promoted to fp64 once per row
+                float af[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int c = 0; c < M; c += 4) {
                     const int h = c / AT, cc = c % AT;
@@ -164,7 +167,7 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
                         float2 R;
                         if constexpr (OP == OP_INTENSITY) {
                             const float r = (W.x * W.x + W.y * W.y) - A;
-                            acc += (double)r * (double)r;
+                            af[q] = fmaf(r, r, af[q]);
                             R = make_float2(W.x * r, W.y * r);
                         } else {
                             const float m2 = W.x * W.x + W.y * W.y;
@@ -172,12 +175,13 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
                             const bool nz = m2 > 0.f;
                             const float mag = nz ? m2 * inv : 0.f;
                             const float dl = mag - A;
-                            acc += (double)dl * (double)dl;
+                            af[q] = fmaf(dl, dl, af[q]);
                             R = nz ? cscale(W, 1.f - A * inv) : make_float2(-A, 0.f);
                         }
                         x[c + q] = make_float2(R.x, -R.y);   // conj
                     }
                 }
+                acc = ((double)af[0] + (double)af[1]) + ((double)af[2] + (double)af[3]);
             }
         } else if (pass == 2) {
             // rows -> columns (x holds conj of the row-inverse; conjugations cancel)

@@ -277,44 +277,9 @@ FrameArgs<T> frame_args(Plan& p, const void* z, const T* amp) {
     return a;
 }
 
-// value = sum_j misfit_j - sum_t dotp_t by 256 threads: fixed contiguous
-// partition + fixed shuffle tree + fixed warp order (deterministic)
 __device__ __forceinline__ void finalize_block(const double* misfit, int N, const double* dotp, int ndot,
                                                double* out, double* red, int lin) {
-    double m = 0.0, d = 0.0;
-    const int cm = (N + 255) / 256, cd = (ndot + 255) / 256;
-    // loads batched ahead of the (in-order) sums: one L2 round trip per 8 values
-    constexpr int B = 8;
-    for (int i = lin * cm, e = min(i + cm, N); i < e; i += B) {
-        double t[B];
-#pragma unroll
-        for (int u = 0; u < B; ++u) t[u] = i + u < e ? __ldcg(misfit + i + u) : 0.0;
-#pragma unroll
-        for (int u = 0; u < B; ++u) m += t[u];
-    }
-    for (int i = lin * cd, e = min(i + cd, ndot); i < e; i += B) {
-        double t[B];
-#pragma unroll
-        for (int u = 0; u < B; ++u) t[u] = i + u < e ? __ldcg(dotp + i + u) : 0.0;
-#pragma unroll
-        for (int u = 0; u < B; ++u) d += t[u];
-    }
-    double both[2] = {m, d};
-    double res[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        double x = both[q];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        __syncthreads();
-        if ((lin & 31) == 0) red[lin >> 5] = x;
-        __syncthreads();
-        double s = 0.0;
-        if (lin == 0)
-            for (int i = 0; i < 8; ++i) s += red[i];
-        res[q] = s;
-    }
-    if (lin == 0) *out = res[0] - res[1];
+    finalize_value<256>(misfit, N, dotp, ndot, out, red, lin);
 }
 
 // ------------------------------------------------------ colour-plane reduce

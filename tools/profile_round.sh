@@ -13,6 +13,6 @@ $CMD > $OUT/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launch.log 2>&1
 echo "launch list rc=$?"
 $CMD > $OUT/plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"frame_tma|overlap_gather" -s 6 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:"frame_tma|overlap_gather|plane_reduce" -s 6 -c 2 \
     -o $OUT/prof_full $CMD > $OUT/ncu_full.log 2>&1
 echo "full capture rc=$?"
