@@ -74,6 +74,13 @@ __device__ __forceinline__ float2 ldg_pinned(const float2* p) {
     return v;
 }
 
+// 1/sqrt(x) as one MUFU op (approximate, flush-to-zero; callers keep x normal)
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // ------------------------------------------------------ register line FFT
 // Compile-time twiddles: Taylor series evaluated by the compiler (constexpr),
 // argument reduced to [-pi, pi]; exact to ~1e-16, rounded once to fp32.

@@ -61,6 +61,14 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
         : "memory");
 }
 
+// epilogue value sc * conj(P) * IDFT_u(R) from x = conj(IDFT_u(R)):
+// conj(P) (sc conj x), scalar FMAs with the signs in the operands
+__device__ __forceinline__ float2 epi_contrib(float2 x, float2 P, float sc) {
+    const float a = x.x * sc, b = x.y * sc;
+    return make_float2(fmaf(P.x, a, -(P.y * b)), fmaf(-P.x, b, -(P.y * a)));
+}
+__device__ __forceinline__ float2 epi_contrib(float2 x, float sc) { return make_float2(x.x * sc, -x.y * sc); }
+
 template <int M, int OP, bool PROBE>
 __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
     frame_tma_kernel(FrameArgs<float> a, int count, const __grid_constant__ CUtensorMap tm_z,
@@ -170,13 +178,16 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
                             af[q] = fmaf(r, r, af[q]);
                             R = make_float2(W.x * r, W.y * r);
                         } else {
-                            const float m2 = W.x * W.x + W.y * W.y;
-                            const float inv = rsqrtf(m2);
-                            const bool nz = m2 > 0.f;
-                            const float mag = nz ? m2 * inv : 0.f;
-                            const float dl = mag - A;
+                            // |W|^2 below the smallest normal float is treated as W = 0
+                            // (theta(0) = 0 branch: R = -A); this keeps the reciprocal
+                            // square root a single flush-to-zero MUFU op
+                            const float m2 = fmaf(W.x, W.x, W.y * W.y);
+                            const bool nz = m2 >= 1.17549435e-38f;
+                            const float inv = nz ? rsqrt_ftz(m2) : 0.f;   // 1/|W|, 0 for W = 0
+                            const float dl = fmaf(m2, inv, -A);            // |W| - A
                             af[q] = fmaf(dl, dl, af[q]);
-                            R = nz ? cscale(W, 1.f - A * inv) : make_float2(-A, 0.f);
+                            const float s = fmaf(-A, inv, 1.f);            // 1 - A/|W|
+                            R = make_float2(fmaf(W.x, s, nz ? 0.f : -A), W.y * s);
                         }
                         x[c + q] = make_float2(R.x, -R.y);   // conj
                     }
@@ -233,8 +244,7 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
             float2* __restrict__ pl = a.planes + (size_t)a.color[j] * a.n * a.n + (size_t)pj.x * a.n + pj.y + t;
 #pragma unroll
             for (int r = 0; r < M; ++r) {
-                float2 v = make_float2(x[r].x * sc, -x[r].y * sc);
-                if constexpr (PROBE) v = cmulc(buf[r * M + t], v);
+                const float2 v = PROBE ? epi_contrib(x[r], buf[r * M + t], sc) : epi_contrib(x[r], sc);
                 pl[(size_t)r * a.n] = v;
             }
             return;
@@ -242,8 +252,8 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
         float2* __restrict__ out = a.stash + (size_t)j * M * S;
 #pragma unroll
         for (int r = 0; r < M; ++r) {
-            float2 v = make_float2(x[r].x * sc, -x[r].y * sc);   // sc * IDFT_u(R)
-            if constexpr (PROBE) v = cmulc(buf[r * M + t], v);   // probe tile (dense pitch M)
+            // probe tile (dense pitch M)
+            const float2 v = PROBE ? epi_contrib(x[r], buf[r * M + t], sc) : epi_contrib(x[r], sc);
             out[(size_t)r * S + odd + t] = v;
         }
         // the two zero pads of row t
