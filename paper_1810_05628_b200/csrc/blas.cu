@@ -78,12 +78,8 @@ __global__ void __launch_bounds__(kReduceThreads) k_dot(const cplx<T>* a, const 
     const size_t lo = blockIdx.x * chunk;
     const size_t hi = lo + chunk < len ? lo + chunk : len;
     double s = 0.0;
-    for (size_t i = lo + threadIdx.x; i < hi; i += kReduceThreads) {
-        const cplx<T> u = a[i], v = b[i];
-        s += (double)u.x * (double)v.x + (double)u.y * (double)v.y;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    for (size_t i = lo + threadIdx.x; i < hi; i += kReduceThreads) s = __dadd_rn(s, dot_term(a[i], b[i]));
+    s = warp_tree(s);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -101,8 +97,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_dot(const cplx<T>* a, const 
         double t = 0.0;
         for (int i = threadIdx.x; i < kReduceBlocks; i += kReduceThreads)
             t += __ldcg(scratch + i);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        t = warp_tree(t);
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
         __syncthreads();
         if (threadIdx.x == 0) {

@@ -46,6 +46,22 @@ void dev_real_convert(int dst_prec, void* dst, int src_dtype, const void* src, s
 constexpr int kReduceBlocks = 592;   // 4 x 148 SMs, fixed => deterministic
 constexpr int kReduceThreads = 256;
 
+// one term of the real inner product <u, v>_R in fp64 with explicit rounding,
+// so every kernel that reduces over the kReduceBlocks partition (k_dot, the
+// fused LBFGS kernels) produces the same bits for the same operands
+template <typename C>
+__device__ __forceinline__ double dot_term(const C& u, const C& v) {
+    return __fma_rn((double)u.x, (double)v.x, __dmul_rn((double)u.y, (double)v.y));
+}
+
+// fixed xor-shuffle tree over a warp (every lane gets the same sum); groups
+// then add their warp sums in warp order
+__device__ __forceinline__ double warp_tree(double s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
 extern thread_local int64_t* g_launch_counter;   // per-plan counter hook
 inline void count_launch(int k = 1) { if (g_launch_counter) *g_launch_counter += k; }
 

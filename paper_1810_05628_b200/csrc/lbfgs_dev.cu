@@ -1,0 +1,276 @@
+// lbfgs_dev.cu — device-resident LBFGS building blocks (see solvers.cuh).
+//
+// The reference's two-loop recursion (solvers.cpp:19-36) is a chain of 2k+2
+// dependent inner products, each followed by an axpy.  Issued as separate
+// kernels with a host read per product it costs ~2k+2 PCIe round trips per
+// iteration; here it is ONE cooperative kernel: every product is reduced over
+// the same fixed kReduceBlocks partition and trees as k_dot (blas.cu), the
+// partials are exchanged through a double-buffered scratch with one grid
+// barrier per product, and every block forms the identical total, so the
+// direction is bitwise the one the kernel-per-op sequence produces.  The
+// curvature-pair bookkeeping (s, y, <s,y>, |s|^2, |y|^2, |g|^2) is one more
+// fused kernel whose four products are read back in a single transfer.
+#include <cooperative_groups.h>
+
+#include "solvers.cuh"
+
+namespace ptg {
+
+namespace {
+
+constexpr int kTlThreads = 1024;                                  // 4 groups of 256 = 4 chunks per block
+constexpr int kTlGroups = kTlThreads / kReduceThreads;
+constexpr int kTlBlocks = kReduceBlocks / kTlGroups;              // 148
+
+template <typename T>
+struct TwoLoopArgs {
+    const cplx<T>* s[kMaxPairs];
+    const cplx<T>* y[kMaxPairs];
+    double sy[kMaxPairs];
+    int k;
+    const cplx<T>* g;
+    cplx<T>* q;
+    double* scratch;   // 2 x kReduceBlocks
+    size_t len;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kTlThreads, 1) k_two_loop(const TwoLoopArgs<T> a) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    using C = cplx<T>;
+    __shared__ double red[kTlThreads / 32];
+    __shared__ double total_s;
+    __shared__ double alpha_s[kMaxPairs];
+    const int sub = threadIdx.x / kReduceThreads, lt = threadIdx.x % kReduceThreads;
+    const int lane = lt & 31, w = lt >> 5;
+    const int c = blockIdx.x * kTlGroups + sub;   // this group's chunk = k_dot's block c
+    const size_t chunk = (a.len + kReduceBlocks - 1) / kReduceBlocks;
+    const size_t lo = min(a.len, (size_t)c * chunk), hi = min(a.len, lo + chunk);
+    int buf = 0;
+
+    // group partial of chunk c (k_dot's block partial) -> scratch, then barrier
+    auto publish = [&](double s) {
+        s = warp_tree(s);
+        if (lane == 0) red[sub * 8 + w] = s;
+        __syncthreads();
+        if (lt == 0) {
+            double t = 0.0;
+            for (int i = 0; i < 8; ++i) t += red[sub * 8 + i];
+            a.scratch[buf * kReduceBlocks + c] = t;
+        }
+        grid.sync();
+    };
+    // k_dot's last-block sum over the partials, formed identically in every block
+    auto total = [&]() -> double {
+        if (sub == 0) {
+            double t = 0.0;
+            for (int i = lt; i < kReduceBlocks; i += kReduceThreads) t += __ldcg(a.scratch + buf * kReduceBlocks + i);
+            t = warp_tree(t);
+            if (lane == 0) red[w] = t;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double u = 0.0;
+            for (int i = 0; i < 8; ++i) u += red[i];
+            total_s = u;
+        }
+        __syncthreads();
+        const double r = total_s;
+        buf ^= 1;
+        return r;
+    };
+
+    const int k = a.k;
+    double p = 0.0;
+    if (k == 0) {   // steepest descent: q = -g
+        for (size_t i = lo + lt; i < hi; i += kReduceThreads) {
+            const C u = a.g[i];
+            const C v = mk<T>(u.x * T(-1), u.y * T(-1));
+            a.q[i] = v;
+            p = __dadd_rn(p, dot_term(v, u));
+        }
+    } else {
+        // q = g ; first product <s_{k-1}, q>
+        for (size_t i = lo + lt; i < hi; i += kReduceThreads) {
+            const C u = a.g[i];
+            a.q[i] = u;
+            p = __dadd_rn(p, dot_term(a.s[k - 1][i], u));
+        }
+        publish(p);
+        // first loop (newest to oldest): alpha_j = <s_j, q>/sy_j ; q -= alpha_j y_j
+        for (int j = k - 1; j >= 0; --j) {
+            const double al = total() / a.sy[j];
+            if (threadIdx.x == 0) alpha_s[j] = al;
+            const T coef = (T)(-al);
+            p = 0.0;
+            for (size_t i = lo + lt; i < hi; i += kReduceThreads) {
+                C v = a.q[i];
+                const C u = a.y[j][i];
+                v.x += coef * u.x;
+                v.y += coef * u.y;
+                a.q[i] = v;
+                p = __dadd_rn(p, j > 0 ? dot_term(a.s[j - 1][i], v) : dot_term(a.y[k - 1][i], a.y[k - 1][i]));
+            }
+            publish(p);
+        }
+        // H0 = gamma I, gamma = sy_new / <y_new, y_new>
+        const T gs = (T)(a.sy[k - 1] / total());
+        p = 0.0;
+        for (size_t i = lo + lt; i < hi; i += kReduceThreads) {
+            const C u = a.q[i];
+            const C v = mk<T>(u.x * gs, u.y * gs);
+            a.q[i] = v;
+            p = __dadd_rn(p, dot_term(a.y[0][i], v));
+        }
+        publish(p);
+        __syncthreads();   // alpha_s visible block-wide
+        // second loop (oldest to newest): beta = <y_j, q>/sy_j ; q += (alpha_j - beta) s_j ; then q = -q
+        for (int j = 0; j < k; ++j) {
+            const double beta = total() / a.sy[j];
+            const T coef = (T)(alpha_s[j] - beta);
+            p = 0.0;
+            for (size_t i = lo + lt; i < hi; i += kReduceThreads) {
+                C v = a.q[i];
+                const C u = a.s[j][i];
+                v.x += coef * u.x;
+                v.y += coef * u.y;
+                if (j + 1 < k) {
+                    a.q[i] = v;
+                    p = __dadd_rn(p, dot_term(a.y[j + 1][i], v));
+                } else {
+                    v = mk<T>(v.x * T(-1), v.y * T(-1));
+                    a.q[i] = v;
+                    p = __dadd_rn(p, dot_term(v, a.g[i]));
+                }
+            }
+            if (j + 1 < k) publish(p);
+        }
+    }
+    // descent check (solvers.cpp:107): <d, g> >= 0 -> d = -g
+    publish(p);
+    if (total() >= 0.0) {
+        for (size_t i = lo + lt; i < hi; i += kReduceThreads) {
+            const C u = a.g[i];
+            a.q[i] = mk<T>(u.x * T(-1), u.y * T(-1));
+        }
+    }
+}
+
+// s = nz - z, y = ng - g and <s,y>, <s,s>, <y,y>, <ng,ng> over k_dot's partition
+template <typename T>
+__global__ void __launch_bounds__(kReduceThreads) k_pair_stats(const cplx<T>* nz, const cplx<T>* z,
+                                                               const cplx<T>* ng, const cplx<T>* g,
+                                                               cplx<T>* s_out, cplx<T>* y_out, size_t len,
+                                                               double* scratch, double* out) {
+    __shared__ double red[4][kReduceThreads / 32];
+    __shared__ bool last;
+    const size_t chunk = (len + kReduceBlocks - 1) / kReduceBlocks;
+    const size_t lo = min(len, (size_t)blockIdx.x * chunk), hi = min(len, lo + chunk);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (size_t i = lo + threadIdx.x; i < hi; i += kReduceThreads) {
+        const cplx<T> s = csub(nz[i], z[i]), y = csub(ng[i], g[i]), gn = ng[i];
+        s_out[i] = s;
+        y_out[i] = y;
+        acc[0] = __dadd_rn(acc[0], dot_term(s, y));
+        acc[1] = __dadd_rn(acc[1], dot_term(s, s));
+        acc[2] = __dadd_rn(acc[2], dot_term(y, y));
+        acc[3] = __dadd_rn(acc[3], dot_term(gn, gn));
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const double t = warp_tree(acc[q]);
+        if (lane == 0) red[q][w] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double t = 0.0;
+        for (int i = 0; i < kReduceThreads / 32; ++i) t += red[threadIdx.x][i];
+        scratch[threadIdx.x * kReduceBlocks + blockIdx.x] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        unsigned int* ctr = reinterpret_cast<unsigned int*>(scratch + 4 * kReduceBlocks);
+        last = atomicAdd(ctr, 1u) == kReduceBlocks - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int q = 0; q < 4; ++q) {
+        double t = 0.0;
+        for (int i = threadIdx.x; i < kReduceBlocks; i += kReduceThreads) t += __ldcg(scratch + q * kReduceBlocks + i);
+        t = warp_tree(t);
+        __syncthreads();
+        if (lane == 0) red[0][w] = t;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double u = 0.0;
+            for (int i = 0; i < kReduceThreads / 32; ++i) u += red[0][i];
+            out[q] = u;
+        }
+    }
+    if (threadIdx.x == 0) *reinterpret_cast<unsigned int*>(scratch + 4 * kReduceBlocks) = 0u;
+}
+
+template <typename T>
+bool two_loop_fits() {
+    static int ok = -1;
+    if (ok < 0) {
+        int dev = 0, sms = 0, per_sm = 0, coop = 0;
+        PTG_CUDA(cudaGetDevice(&dev));
+        PTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        PTG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+        PTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_two_loop<T>, kTlThreads, 0));
+        ok = coop && per_sm * sms >= kTlBlocks;
+    }
+    return ok == 1;
+}
+
+template <typename T>
+bool launch_two_loop(const Plan& p, const void* const* s, const void* const* y, const double* sy, int k,
+                     const void* g, void* q, double* scratch) {
+    if (k > kMaxPairs || !two_loop_fits<T>()) return false;
+    TwoLoopArgs<T> a{};
+    for (int i = 0; i < k; ++i) {
+        a.s[i] = static_cast<const cplx<T>*>(s[i]);
+        a.y[i] = static_cast<const cplx<T>*>(y[i]);
+        a.sy[i] = sy[i];
+    }
+    a.k = k;
+    a.g = static_cast<const cplx<T>*>(g);
+    a.q = static_cast<cplx<T>*>(q);
+    a.scratch = scratch;
+    a.len = p.nn();
+    void* args[] = {&a};
+    PTG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_two_loop<T>), dim3(kTlBlocks),
+                                         dim3(kTlThreads), args, 0, p.stream));
+    count_launch();
+    return true;
+}
+
+}  // namespace
+
+bool dev_two_loop(const Plan& p, const void* const* s, const void* const* y, const double* sy, int k,
+                  const void* g, void* q, double* scratch) {
+    return p.prec == PTG_C64 ? launch_two_loop<float>(p, s, y, sy, k, g, q, scratch)
+                             : launch_two_loop<double>(p, s, y, sy, k, g, q, scratch);
+}
+
+void dev_pair_stats(const Plan& p, const void* nz, const void* z, const void* ng, const void* g, void* s_out,
+                    void* y_out, double* scratch, double* out_dev) {
+    const size_t len = p.nn();
+    if (p.prec == PTG_C64)
+        k_pair_stats<float><<<kReduceBlocks, kReduceThreads, 0, p.stream>>>(
+            (const float2*)nz, (const float2*)z, (const float2*)ng, (const float2*)g, (float2*)s_out, (float2*)y_out,
+            len, scratch, out_dev);
+    else
+        k_pair_stats<double><<<kReduceBlocks, kReduceThreads, 0, p.stream>>>(
+            (const double2*)nz, (const double2*)z, (const double2*)ng, (const double2*)g, (double2*)s_out,
+            (double2*)y_out, len, scratch, out_dev);
+    PTG_CHECK_LAUNCH();
+    count_launch();
+}
+
+}  // namespace ptg

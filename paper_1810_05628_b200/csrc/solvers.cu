@@ -1,51 +1,57 @@
 // solvers.cu — GPU-resident line search / LBFGS / MG/OPT (see solvers.cuh).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "solvers.cuh"
 #include "transfer.cuh"
 
 namespace ptg {
 
-double DObj::eval(Counter& c, const void* z, void* grad) const {
+double DObj::eval(Counter& c, const void* z, void* grad) const { return eval_checked(c, z, grad, nullptr); }
+
+double DObj::eval_checked(Counter& c, const void* z, void* grad, bool* nonfinite) const {
+    Plan& p = *plan;
+    LaunchScope ls(p);
     c.record(level, weight);   // charge before evaluating (solvers.hpp:33-36)
-    plan_eval(*plan, metric, z, v, grad, plan->value.as<double>());
-    return plan_read_scalar(*plan, plan->value.as<double>());
+    if (nonfinite) dev_nonfinite(p.prec, z, p.nn(), p.flag.as<int>(), p.stream);
+    plan_eval(p, metric, z, v, grad, p.value.as<double>());
+    double* h = p.hval.as<double>();
+    PTG_CUDA(cudaMemcpyAsync(h, p.value.p, sizeof(double), cudaMemcpyDeviceToHost, p.stream));
+    if (nonfinite) PTG_CUDA(cudaMemcpyAsync(h + 1, p.flag.p, sizeof(int), cudaMemcpyDeviceToHost, p.stream));
+    PTG_CUDA(cudaStreamSynchronize(p.stream));
+    if (nonfinite) *nonfinite = *reinterpret_cast<const int*>(h + 1) != 0;
+    return h[0];
 }
 
 static double dnorm(Plan& p, const void* a) { return std::sqrt(plan_dot(p, a, a, p.nn())); }
 
 LsOut d_linesearch(const DObj& obj, const void* z, const void* dir, Counter& ctr, int max_trials,
-                   const double* phi0, void* z_out, void* g_out) {
+                   const double* phi0, void* z_out, void* g_out, bool check_finite) {
     Plan& p = *obj.plan;
     LaunchScope ls(p);
     const size_t len = p.nn();
     LsOut r;
-    double base;
-    if (phi0) {
-        base = *phi0;
-    } else {
-        DVec tmp(p, len);
-        base = obj.eval(ctr, z, tmp.p);
-    }
-    DVec trial(p, len), g(p, len);
+    // g_out doubles as the gradient scratch of the base evaluation
+    const double base = phi0 ? *phi0 : obj.eval(ctr, z, g_out);
     double alpha = 1.0;
     for (int t = 0; t < max_trials; ++t) {
-        dev_add_scaled(p.prec, trial.p, z, alpha, dir, len, p.stream);   // z + alpha d
-        const double v = obj.eval(ctr, trial.p, g.p);
+        dev_add_scaled(p.prec, z_out, z, alpha, dir, len, p.stream);   // z + alpha d
+        bool nf = false;
+        const double v = obj.eval_checked(ctr, z_out, g_out, check_finite ? &nf : nullptr);
         ++r.trials;
         if (v <= base) {
             r.alpha = alpha;
             r.value = v;
-            dev_copy(p.prec, z_out, trial.p, len, p.stream);
-            dev_copy(p.prec, g_out, g.p, len, p.stream);
+            r.nonfinite = nf;
             return r;
         }
         alpha *= 0.5;
     }
     r.alpha = 0.0;
     r.stalled = true;
-    if (z_out != z) dev_copy(p.prec, z_out, z, len, p.stream);
+    dev_copy(p.prec, z_out, z, len, p.stream);
     return r;
 }
 
@@ -55,25 +61,26 @@ struct Pair {
     double sy;
 };
 
-// solvers.cpp:19-36
-void two_loop(Plan& p, const std::deque<Pair>& pairs, const void* g, void* q) {
-    const size_t len = p.nn();
-    if (pairs.empty()) {
+// solvers.cpp:19-36, one kernel per operation with a host read per product
+// (fallback of the fused dev_two_loop; same arithmetic, same bits)
+void two_loop(Plan& p, const std::vector<const void*>& s, const std::vector<const void*>& y,
+              const std::vector<double>& sy, const void* g, void* q) {
+    const size_t len = p.nn(), k = s.size();
+    if (k == 0) {
         dev_scale(p.prec, q, g, -1.0, len, p.stream);
         return;
     }
     dev_copy(p.prec, q, g, len, p.stream);
-    std::vector<double> alpha(pairs.size());
-    for (size_t i = pairs.size(); i-- > 0;) {
-        alpha[i] = plan_dot(p, pairs[i].s.p, q, len) / pairs[i].sy;
-        dev_axpy(p.prec, q, -alpha[i], pairs[i].y.p, len, p.stream);
+    std::vector<double> alpha(k);
+    for (size_t i = k; i-- > 0;) {
+        alpha[i] = plan_dot(p, s[i], q, len) / sy[i];
+        dev_axpy(p.prec, q, -alpha[i], y[i], len, p.stream);
     }
-    const Pair& newest = pairs.back();
-    const double gamma = newest.sy / plan_dot(p, newest.y.p, newest.y.p, len);
+    const double gamma = sy[k - 1] / plan_dot(p, y[k - 1], y[k - 1], len);
     dev_scale(p.prec, q, q, gamma, len, p.stream);
-    for (size_t i = 0; i < pairs.size(); ++i) {
-        const double beta = plan_dot(p, pairs[i].y.p, q, len) / pairs[i].sy;
-        dev_axpy(p.prec, q, alpha[i] - beta, pairs[i].s.p, len, p.stream);
+    for (size_t i = 0; i < k; ++i) {
+        const double beta = plan_dot(p, y[i], q, len) / sy[i];
+        dev_axpy(p.prec, q, alpha[i] - beta, s[i], len, p.stream);
     }
     dev_scale(p.prec, q, q, -1.0, len, p.stream);
 }
@@ -102,31 +109,68 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     auto satisfied = [&](double gn) { return gn <= std::max(cfg.grad_tol_rel * g0, grad_floor); };
     SolveOut out;
     out.reason = PTG_STOP_MAXITERS;
-    std::deque<Pair> pairs;   // fresh memory per call (solvers.cpp:100)
+    // Curvature pairs live in a ring of slots allocated on first use (memory+1:
+    // a candidate pair is formed before its acceptance is known); the order
+    // deque holds slot ids oldest..newest.  Fresh memory per call (solvers.cpp:100).
+    const int mem = std::max(0, cfg.lbfgs_memory);
+    std::vector<Pair> slots;
+    std::deque<int> order;
+    DVec ws;   // fused-kernel scratch: 4 x kReduceBlocks partials + counter, 4 results
+    double* wsd = nullptr;
+    double* stats_h = p.hval.as<double>();
+    // PTG_TWO_LOOP=ops selects the kernel-per-op two-loop (equivalence tests, A/B)
+    const char* tl = getenv("PTG_TWO_LOOP");
+    bool fused = !(tl && std::string(tl) == "ops");
     if (satisfied(gnorm)) {
         out.reason = PTG_STOP_TOLERANCE;
     } else {
+        ws.s = p.stream;
+        ws.bytes = (4 * kReduceBlocks + 8) * sizeof(double);
+        PTG_CUDA(cudaMallocAsync(&ws.p, ws.bytes, p.stream));
+        PTG_CUDA(cudaMemsetAsync(ws.p, 0, ws.bytes, p.stream));
+        wsd = static_cast<double*>(ws.p);
         for (int iter = 1; iter <= cfg.max_iters; ++iter) {
-            two_loop(p, pairs, g.p, dir.p);
-            if (plan_dot(p, dir.p, g.p, len) >= 0.0) dev_scale(p.prec, dir.p, g.p, -1.0, len, p.stream);
-            LsOut lsr = d_linesearch(obj, z.p, dir.p, ctr, cfg.linesearch_max, &cur, nz.p, ng.p);
+            // direction: fused two-loop + descent check, else the kernel-per-op path
+            std::vector<const void*> sp, yp;
+            std::vector<double> syv;
+            for (int id : order) {
+                sp.push_back(slots[id].s.p);
+                yp.push_back(slots[id].y.p);
+                syv.push_back(slots[id].sy);
+            }
+            fused = fused && dev_two_loop(p, sp.data(), yp.data(), syv.data(), (int)order.size(), g.p, dir.p, wsd);
+            if (!fused) {
+                two_loop(p, sp, yp, syv, g.p, dir.p);
+                if (plan_dot(p, dir.p, g.p, len) >= 0.0) dev_scale(p.prec, dir.p, g.p, -1.0, len, p.stream);
+            }
+            LsOut lsr = d_linesearch(obj, z.p, dir.p, ctr, cfg.linesearch_max, &cur, nz.p, ng.p, true);
             if (lsr.stalled) {
                 out.reason = PTG_STOP_STALL;
                 break;
             }
-            if (plan_nonfinite(p, nz.p, len)) raise(PTG_ERR_NUMERIC, "non-finite iterate in lbfgs");
-            Pair pr{DVec(p, len), DVec(p, len), 0.0};
-            dev_sub(p.prec, pr.s.p, nz.p, z.p, len, p.stream);
-            dev_sub(p.prec, pr.y.p, ng.p, g.p, len, p.stream);
-            pr.sy = plan_dot(p, pr.s.p, pr.y.p, len);
-            if (pr.sy > 1e-12 * dnorm(p, pr.s.p) * dnorm(p, pr.y.p)) {
-                pairs.push_back(std::move(pr));
-                if ((int)pairs.size() > cfg.lbfgs_memory) pairs.pop_front();
+            if (lsr.nonfinite) raise(PTG_ERR_NUMERIC, "non-finite iterate in lbfgs");
+            // candidate pair into a free slot
+            int slot = -1;
+            for (int i = 0; i < (int)slots.size() && slot < 0; ++i)
+                if (std::find(order.begin(), order.end(), i) == order.end()) slot = i;
+            if (slot < 0) {
+                slots.push_back(Pair{DVec(p, len), DVec(p, len), 0.0});
+                slot = (int)slots.size() - 1;
+            }
+            Pair& pr = slots[slot];
+            dev_pair_stats(p, nz.p, z.p, ng.p, g.p, pr.s.p, pr.y.p, wsd, wsd + 4 * kReduceBlocks + 2);
+            PTG_CUDA(cudaMemcpyAsync(stats_h, wsd + 4 * kReduceBlocks + 2, 4 * sizeof(double),
+                                     cudaMemcpyDeviceToHost, p.stream));
+            PTG_CUDA(cudaStreamSynchronize(p.stream));
+            pr.sy = stats_h[0];
+            if (pr.sy > 1e-12 * std::sqrt(stats_h[1]) * std::sqrt(stats_h[2])) {
+                order.push_back(slot);
+                if ((int)order.size() > mem) order.pop_front();
             }
             std::swap(z, nz);
             std::swap(g, ng);
             cur = lsr.value;
-            gnorm = dnorm(p, g.p);
+            gnorm = std::sqrt(stats_h[3]);
             if (hist) hist->push_back({ctr.weighted, cur, gnorm});
             if (satisfied(gnorm)) {
                 out.reason = PTG_STOP_TOLERANCE;

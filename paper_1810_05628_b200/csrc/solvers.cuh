@@ -68,6 +68,9 @@ struct DObj {
     int level = 0;
     double weight = 1.0;
     double eval(Counter& c, const void* z, void* grad) const;
+    // eval + (optionally) the ComplexField::isFinite test of z, read back in
+    // the same transfer as the value
+    double eval_checked(Counter& c, const void* z, void* grad, bool* nonfinite) const;
 };
 
 struct SolveOut {
@@ -75,14 +78,30 @@ struct SolveOut {
     int reason = PTG_STOP_MAXITERS;
 };
 
-// solvers.cpp:61-85; writes the accepted point into z_out/g_out
+// solvers.cpp:61-85; trials are formed in z_out (gradient in g_out), so the
+// accepted point needs no copy; on a stall z_out = z and g_out is scratch.
+// z_out / g_out must not alias z / dir.
 struct LsOut {
     double alpha = 0.0, value = 0.0;
     bool stalled = false;
+    bool nonfinite = false;   // accepted point failed isFinite (only with check_finite)
     int trials = 0;
 };
 LsOut d_linesearch(const DObj& obj, const void* z, const void* dir, Counter& ctr, int max_trials,
-                   const double* phi0, void* z_out, void* g_out);
+                   const double* phi0, void* z_out, void* g_out, bool check_finite = false);
+
+// fused LBFGS kernels (lbfgs_dev.cu)
+constexpr int kMaxPairs = 64;
+// q = -H g by the two-loop recursion over pairs (s[i], y[i], sy[i]) oldest..newest,
+// then the descent check (<q,g> >= 0 -> q = -g); one cooperative launch.
+// scratch: 2 x kReduceBlocks doubles.  false = not launched (too many pairs /
+// device cannot co-schedule the grid): use the kernel-per-op path.
+bool dev_two_loop(const Plan& p, const void* const* s, const void* const* y, const double* sy, int k,
+                  const void* g, void* q, double* scratch);
+// s = nz - z, y = ng - g; out_dev[0..3] = <s,y>, <s,s>, <y,y>, <ng,ng>
+// scratch: 4 x kReduceBlocks doubles + a zeroed counter
+void dev_pair_stats(const Plan& p, const void* nz, const void* z, const void* ng, const void* g, void* s_out,
+                    void* y_out, double* scratch, double* out_dev);
 
 // solvers.cpp:87-141.  warm_g (device) with *warm_value, or null to evaluate.
 SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Counter& ctr,

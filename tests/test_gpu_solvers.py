@@ -156,3 +156,17 @@ def test_lbfgs_budget_and_stall(oracle):
     assert r.reason == "budget" and r.weighted_evals >= 5.0
     w = oracle.lbfgs(p, z0, max_iters=50, max_weighted=5.0)
     assert r.weighted_evals == w.weighted
+
+
+@pytest.mark.parametrize("precision", ["c64", "c128"])
+def test_fused_two_loop_matches_per_op(oracle, monkeypatch, precision):
+    """The cooperative two-loop kernel reduces every product over the same
+    partition and trees as the kernel-per-op path: identical bits."""
+    p, plan, cfg = _patch(oracle, precision)
+    z0 = np.ones((cfg.n, cfg.n), np.complex128)
+    a = plan.lbfgs(z0, max_iters=30, lbfgs_memory=5)
+    monkeypatch.setenv("PTG_TWO_LOOP", "ops")
+    b = plan.lbfgs(z0, max_iters=30, lbfgs_memory=5)
+    assert len(a.history) > 6
+    assert np.array_equal(a.final_iterate, b.final_iterate)
+    assert np.array_equal(a.history, b.history)
