@@ -12,6 +12,8 @@
 // fused kernel whose four products are read back in a single transfer.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "solvers.cuh"
 
 namespace ptg {
@@ -33,6 +35,146 @@ struct TwoLoopArgs {
     double* scratch;   // 2 x kReduceBlocks
     size_t len;
 };
+
+// Register-resident two-loop for short chunks (<= 256*QE elements): every
+// thread keeps its q and g elements in registers for the whole recursion,
+// and the operand vectors of the next product are loaded before the barrier
+// of the current one.  Same partition, trees and arithmetic as k_two_loop
+// (and k_dot + k_axpy).
+template <typename T, int QE>
+__global__ void __launch_bounds__(kTlThreads, 1) k_two_loop_reg(const TwoLoopArgs<T> a) {
+    using C = cplx<T>;
+    __shared__ double red[kTlThreads / 32];
+    __shared__ double total_s;
+    __shared__ double alpha_s[kMaxPairs];
+    const int sub = threadIdx.x / kReduceThreads, lt = threadIdx.x % kReduceThreads;
+    const int lane = lt & 31, w = lt >> 5;
+    const int c = blockIdx.x * kTlGroups + sub;
+    const size_t chunk = (a.len + kReduceBlocks - 1) / kReduceBlocks;
+    const size_t lo = min(a.len, (size_t)c * chunk), hi = min(a.len, lo + chunk);
+    unsigned idx[QE];   // 32-bit element offsets (register budget: 64 per thread)
+    bool ok[QE];
+#pragma unroll
+    for (int e = 0; e < QE; ++e) {
+        const size_t i = lo + lt + (size_t)e * kReduceThreads;
+        ok[e] = i < hi;
+        idx[e] = ok[e] ? (unsigned)i : 0u;
+    }
+    const C zero = mk<T>(T(0), T(0));
+    int buf = 0;
+
+    auto load = [&](const C* v, C (&r)[QE]) {
+#pragma unroll
+        for (int e = 0; e < QE; ++e) r[e] = ok[e] ? v[idx[e]] : zero;
+    };
+    auto publish = [&](double s) {
+        s = warp_tree(s);
+        if (lane == 0) red[sub * 8 + w] = s;
+        __syncthreads();
+        if (lt == 0) {
+            double t = 0.0;
+            for (int i = 0; i < 8; ++i) t += red[sub * 8 + i];
+            a.scratch[buf * kReduceBlocks + c] = t;
+        }
+        cooperative_groups::this_grid().sync();
+    };
+    auto total = [&]() -> double {
+        if (sub == 0) {
+            double t = 0.0;
+            for (int i = lt; i < kReduceBlocks; i += kReduceThreads) t += __ldcg(a.scratch + buf * kReduceBlocks + i);
+            t = warp_tree(t);
+            if (lane == 0) red[w] = t;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double u = 0.0;
+            for (int i = 0; i < 8; ++i) u += red[i];
+            total_s = u;
+        }
+        __syncthreads();
+        const double r = total_s;
+        buf ^= 1;
+        return r;
+    };
+    auto dot = [&](const C (&u)[QE], const C (&v)[QE]) {
+        double p = 0.0;
+#pragma unroll
+        for (int e = 0; e < QE; ++e)
+            if (ok[e]) p = __dadd_rn(p, dot_term(u[e], v[e]));
+        return p;
+    };
+
+    const int k = a.k;
+    C qv[QE], u[QE], nx[QE];   // g is re-read where needed (register budget)
+    double p;
+    if (k == 0) {
+        load(a.g, u);
+#pragma unroll
+        for (int e = 0; e < QE; ++e) qv[e] = mk<T>(u[e].x * T(-1), u[e].y * T(-1));
+        p = dot(qv, u);
+    } else {
+        load(a.g, qv);
+        load(a.s[k - 1], nx);
+        p = dot(nx, qv);
+        load(a.y[k - 1], u);                                   // operands of the first axpy
+        load(k > 1 ? a.s[k - 2] : a.y[k - 1], nx);             // and of the next product
+        publish(p);
+        for (int j = k - 1; j >= 0; --j) {
+            const double al = total() / a.sy[j];
+            if (threadIdx.x == 0) alpha_s[j] = al;
+            const T coef = (T)(-al);
+#pragma unroll
+            for (int e = 0; e < QE; ++e) {
+                qv[e].x += coef * u[e].x;
+                qv[e].y += coef * u[e].y;
+            }
+            p = j > 0 ? dot(nx, qv) : dot(nx, nx);
+            if (j > 0) {
+                load(a.y[j - 1], u);
+                load(j > 1 ? a.s[j - 2] : a.y[k - 1], nx);
+            } else {
+                load(a.y[0], nx);                              // gamma pass product
+            }
+            publish(p);
+        }
+        const T gs = (T)(a.sy[k - 1] / total());
+#pragma unroll
+        for (int e = 0; e < QE; ++e) qv[e] = mk<T>(qv[e].x * gs, qv[e].y * gs);
+        p = dot(nx, qv);
+        load(a.s[0], u);
+        load(k > 1 ? a.y[1] : a.g, nx);                        // next product operand (g for the descent check)
+        publish(p);
+        __syncthreads();   // alpha_s visible block-wide
+        for (int j = 0; j < k; ++j) {
+            const double beta = total() / a.sy[j];
+            const T coef = (T)(alpha_s[j] - beta);
+#pragma unroll
+            for (int e = 0; e < QE; ++e) {
+                qv[e].x += coef * u[e].x;
+                qv[e].y += coef * u[e].y;
+            }
+            if (j + 1 < k) {
+                p = dot(nx, qv);
+                load(a.s[j + 1], u);
+                load(j + 2 < k ? a.y[j + 2] : a.g, nx);
+                publish(p);
+            } else {
+#pragma unroll
+                for (int e = 0; e < QE; ++e) qv[e] = mk<T>(qv[e].x * T(-1), qv[e].y * T(-1));
+                p = dot(qv, nx);                               // nx = g
+            }
+        }
+    }
+    publish(p);
+    if (total() >= 0.0) {
+        load(a.g, u);
+#pragma unroll
+        for (int e = 0; e < QE; ++e) qv[e] = mk<T>(u[e].x * T(-1), u[e].y * T(-1));
+    }
+#pragma unroll
+    for (int e = 0; e < QE; ++e)
+        if (ok[e]) a.q[idx[e]] = qv[e];
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kTlThreads, 1) k_two_loop(const TwoLoopArgs<T> a) {
@@ -214,16 +356,22 @@ __global__ void __launch_bounds__(kReduceThreads) k_pair_stats(const cplx<T>* nz
     if (threadIdx.x == 0) *reinterpret_cast<unsigned int*>(scratch + 4 * kReduceBlocks) = 0u;
 }
 
+template <typename K>
+bool coop_fits(K kern) {
+    int dev = 0, sms = 0, per_sm = 0, coop = 0;
+    PTG_CUDA(cudaGetDevice(&dev));
+    PTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    PTG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    PTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTlThreads, 0));
+    return coop && per_sm * sms >= kTlBlocks;
+}
+
 template <typename T>
 bool two_loop_fits() {
     static int ok = -1;
     if (ok < 0) {
-        int dev = 0, sms = 0, per_sm = 0, coop = 0;
-        PTG_CUDA(cudaGetDevice(&dev));
-        PTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        PTG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
-        PTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_two_loop<T>, kTlThreads, 0));
-        ok = coop && per_sm * sms >= kTlBlocks;
+        ok = coop_fits(k_two_loop<T>) && coop_fits(k_two_loop_reg<T, 1>) && coop_fits(k_two_loop_reg<T, 2>);
+        if constexpr (sizeof(T) == 4) ok = ok && coop_fits(k_two_loop_reg<T, 4>);
     }
     return ok == 1;
 }
@@ -244,8 +392,18 @@ bool launch_two_loop(const Plan& p, const void* const* s, const void* const* y, 
     a.scratch = scratch;
     a.len = p.nn();
     void* args[] = {&a};
-    PTG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_two_loop<T>), dim3(kTlBlocks),
-                                         dim3(kTlThreads), args, 0, p.stream));
+    const size_t chunk = (a.len + kReduceBlocks - 1) / kReduceBlocks;
+    size_t qe = (chunk + kReduceThreads - 1) / kReduceThreads;   // elements per thread
+    const void* kern = reinterpret_cast<const void*>(k_two_loop<T>);
+    // PTG_TWO_LOOP=mem: memory-resident variant for any size (A/B)
+    const char* tl = getenv("PTG_TWO_LOOP");
+    if (tl && tl[0] == 'm') qe = ~size_t(0);
+    if (qe <= 1) kern = reinterpret_cast<const void*>(k_two_loop_reg<T, 1>);
+    else if (qe <= 2) kern = reinterpret_cast<const void*>(k_two_loop_reg<T, 2>);
+    else if constexpr (sizeof(T) == 4) {
+        if (qe <= 4) kern = reinterpret_cast<const void*>(k_two_loop_reg<T, 4>);
+    }
+    PTG_CUDA(cudaLaunchCooperativeKernel(kern, dim3(kTlBlocks), dim3(kTlThreads), args, 0, p.stream));
     count_launch();
     return true;
 }
