@@ -299,7 +299,8 @@ __global__ void __launch_bounds__(kTlThreads, 1) k_two_loop(const TwoLoopArgs<T>
     }
 }
 
-// s = nz - z, y = ng - g and <s,y>, <s,s>, <y,y>, <ng,ng> over k_dot's partition
+// s = nz - z, y = ng - g and <s,y>, <s,s>, <y,y>, <ng,ng> over k_dot's
+// partition, plus the isFinite test of nz (ComplexField::isFinite)
 template <typename T>
 __global__ void __launch_bounds__(kReduceThreads) k_pair_stats(const cplx<T>* nz, const cplx<T>* z,
                                                                const cplx<T>* ng, const cplx<T>* g,
@@ -310,8 +311,11 @@ __global__ void __launch_bounds__(kReduceThreads) k_pair_stats(const cplx<T>* nz
     const size_t chunk = (len + kReduceBlocks - 1) / kReduceBlocks;
     const size_t lo = min(len, (size_t)blockIdx.x * chunk), hi = min(len, lo + chunk);
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    bool bad = false;
     for (size_t i = lo + threadIdx.x; i < hi; i += kReduceThreads) {
-        const cplx<T> s = csub(nz[i], z[i]), y = csub(ng[i], g[i]), gn = ng[i];
+        const cplx<T> zn = nz[i];
+        const cplx<T> s = csub(zn, z[i]), y = csub(ng[i], g[i]), gn = ng[i];
+        bad |= !isfinite(zn.x) || !isfinite(zn.y);
         s_out[i] = s;
         y_out[i] = y;
         acc[0] = __dadd_rn(acc[0], dot_term(s, y));
@@ -325,22 +329,23 @@ __global__ void __launch_bounds__(kReduceThreads) k_pair_stats(const cplx<T>* nz
         const double t = warp_tree(acc[q]);
         if (lane == 0) red[q][w] = t;
     }
-    __syncthreads();
+    bad = __syncthreads_or(bad);
     if (threadIdx.x < 4) {
         double t = 0.0;
         for (int i = 0; i < kReduceThreads / 32; ++i) t += red[threadIdx.x][i];
         scratch[threadIdx.x * kReduceBlocks + blockIdx.x] = t;
     }
+    if (threadIdx.x == 4) scratch[4 * kReduceBlocks + blockIdx.x] = bad ? 1.0 : 0.0;
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
-        unsigned int* ctr = reinterpret_cast<unsigned int*>(scratch + 4 * kReduceBlocks);
+        unsigned int* ctr = reinterpret_cast<unsigned int*>(scratch + 5 * kReduceBlocks);
         last = atomicAdd(ctr, 1u) == kReduceBlocks - 1;
     }
     __syncthreads();
     if (!last) return;
     __threadfence();
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < 5; ++q) {
         double t = 0.0;
         for (int i = threadIdx.x; i < kReduceBlocks; i += kReduceThreads) t += __ldcg(scratch + q * kReduceBlocks + i);
         t = warp_tree(t);
@@ -353,7 +358,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_pair_stats(const cplx<T>* nz
             out[q] = u;
         }
     }
-    if (threadIdx.x == 0) *reinterpret_cast<unsigned int*>(scratch + 4 * kReduceBlocks) = 0u;
+    if (threadIdx.x == 0) *reinterpret_cast<unsigned int*>(scratch + 5 * kReduceBlocks) = 0u;
 }
 
 template <typename K>

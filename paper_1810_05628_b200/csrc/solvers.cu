@@ -9,42 +9,42 @@
 
 namespace ptg {
 
-double DObj::eval(Counter& c, const void* z, void* grad) const { return eval_checked(c, z, grad, nullptr); }
-
-double DObj::eval_checked(Counter& c, const void* z, void* grad, bool* nonfinite) const {
+void DObj::eval_enqueue(Counter& c, const void* z, void* grad, double* host_value) const {
     Plan& p = *plan;
-    LaunchScope ls(p);
     c.record(level, weight);   // charge before evaluating (solvers.hpp:33-36)
-    if (nonfinite) dev_nonfinite(p.prec, z, p.nn(), p.flag.as<int>(), p.stream);
     plan_eval(p, metric, z, v, grad, p.value.as<double>());
-    double* h = p.hval.as<double>();
-    PTG_CUDA(cudaMemcpyAsync(h, p.value.p, sizeof(double), cudaMemcpyDeviceToHost, p.stream));
-    if (nonfinite) PTG_CUDA(cudaMemcpyAsync(h + 1, p.flag.p, sizeof(int), cudaMemcpyDeviceToHost, p.stream));
-    PTG_CUDA(cudaStreamSynchronize(p.stream));
-    if (nonfinite) *nonfinite = *reinterpret_cast<const int*>(h + 1) != 0;
+    PTG_CUDA(cudaMemcpyAsync(host_value, p.value.p, sizeof(double), cudaMemcpyDeviceToHost, p.stream));
+}
+
+double DObj::eval(Counter& c, const void* z, void* grad) const {
+    double* h = plan->hval.as<double>();
+    eval_enqueue(c, z, grad, h);
+    PTG_CUDA(cudaStreamSynchronize(plan->stream));
     return h[0];
 }
 
 static double dnorm(Plan& p, const void* a) { return std::sqrt(plan_dot(p, a, a, p.nn())); }
 
 LsOut d_linesearch(const DObj& obj, const void* z, const void* dir, Counter& ctr, int max_trials,
-                   const double* phi0, void* z_out, void* g_out, bool check_finite) {
+                   const double* phi0, void* z_out, void* g_out, const std::function<void()>& first_trial_hook) {
     Plan& p = *obj.plan;
     LaunchScope ls(p);
     const size_t len = p.nn();
     LsOut r;
     // g_out doubles as the gradient scratch of the base evaluation
     const double base = phi0 ? *phi0 : obj.eval(ctr, z, g_out);
+    double* h = p.hval.as<double>();
     double alpha = 1.0;
     for (int t = 0; t < max_trials; ++t) {
         dev_add_scaled(p.prec, z_out, z, alpha, dir, len, p.stream);   // z + alpha d
-        bool nf = false;
-        const double v = obj.eval_checked(ctr, z_out, g_out, check_finite ? &nf : nullptr);
+        obj.eval_enqueue(ctr, z_out, g_out, h);
+        if (t == 0 && first_trial_hook) first_trial_hook();
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+        const double v = h[0];
         ++r.trials;
         if (v <= base) {
             r.alpha = alpha;
             r.value = v;
-            r.nonfinite = nf;
             return r;
         }
         alpha *= 0.5;
@@ -115,9 +115,10 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     const int mem = std::max(0, cfg.lbfgs_memory);
     std::vector<Pair> slots;
     std::deque<int> order;
-    DVec ws;   // fused-kernel scratch: 4 x kReduceBlocks partials + counter, 4 results
+    DVec ws;   // fused-kernel scratch (two-loop partials / pair statistics)
     double* wsd = nullptr;
-    double* stats_h = p.hval.as<double>();
+    p.hval.ensure(8 * sizeof(double));
+    double* stats_h = p.hval.as<double>() + 2;   // [0] = line-search value
     // PTG_TWO_LOOP=ops selects the kernel-per-op two-loop (equivalence tests, A/B)
     const char* tl = getenv("PTG_TWO_LOOP");
     bool fused = !(tl && std::string(tl) == "ops");
@@ -125,10 +126,11 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
         out.reason = PTG_STOP_TOLERANCE;
     } else {
         ws.s = p.stream;
-        ws.bytes = (4 * kReduceBlocks + 8) * sizeof(double);
+        ws.bytes = (size_t)kPairScratch * sizeof(double) + 8 * sizeof(double);
         PTG_CUDA(cudaMallocAsync(&ws.p, ws.bytes, p.stream));
         PTG_CUDA(cudaMemsetAsync(ws.p, 0, ws.bytes, p.stream));
         wsd = static_cast<double*>(ws.p);
+        double* stats_d = wsd + kPairScratch;
         for (int iter = 1; iter <= cfg.max_iters; ++iter) {
             // direction: fused two-loop + descent check, else the kernel-per-op path
             std::vector<const void*> sp, yp;
@@ -143,13 +145,7 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                 two_loop(p, sp, yp, syv, g.p, dir.p);
                 if (plan_dot(p, dir.p, g.p, len) >= 0.0) dev_scale(p.prec, dir.p, g.p, -1.0, len, p.stream);
             }
-            LsOut lsr = d_linesearch(obj, z.p, dir.p, ctr, cfg.linesearch_max, &cur, nz.p, ng.p, true);
-            if (lsr.stalled) {
-                out.reason = PTG_STOP_STALL;
-                break;
-            }
-            if (lsr.nonfinite) raise(PTG_ERR_NUMERIC, "non-finite iterate in lbfgs");
-            // candidate pair into a free slot
+            // candidate pair slot (not in the order deque)
             int slot = -1;
             for (int i = 0; i < (int)slots.size() && slot < 0; ++i)
                 if (std::find(order.begin(), order.end(), i) == order.end()) slot = i;
@@ -158,10 +154,22 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                 slot = (int)slots.size() - 1;
             }
             Pair& pr = slots[slot];
-            dev_pair_stats(p, nz.p, z.p, ng.p, g.p, pr.s.p, pr.y.p, wsd, wsd + 4 * kReduceBlocks + 2);
-            PTG_CUDA(cudaMemcpyAsync(stats_h, wsd + 4 * kReduceBlocks + 2, 4 * sizeof(double),
-                                     cudaMemcpyDeviceToHost, p.stream));
-            PTG_CUDA(cudaStreamSynchronize(p.stream));
+            // pair statistics (+ isFinite of the new iterate) of the accepted point,
+            // enqueued speculatively behind the first trial's evaluation
+            auto stats = [&]() {
+                dev_pair_stats(p, nz.p, z.p, ng.p, g.p, pr.s.p, pr.y.p, wsd, stats_d);
+                PTG_CUDA(cudaMemcpyAsync(stats_h, stats_d, 5 * sizeof(double), cudaMemcpyDeviceToHost, p.stream));
+            };
+            LsOut lsr = d_linesearch(obj, z.p, dir.p, ctr, cfg.linesearch_max, &cur, nz.p, ng.p, stats);
+            if (lsr.stalled) {
+                out.reason = PTG_STOP_STALL;
+                break;
+            }
+            if (lsr.trials > 1) {   // the speculative statistics were for a rejected trial
+                stats();
+                PTG_CUDA(cudaStreamSynchronize(p.stream));
+            }
+            if (stats_h[4] != 0.0) raise(PTG_ERR_NUMERIC, "non-finite iterate in lbfgs");
             pr.sy = stats_h[0];
             if (pr.sy > 1e-12 * std::sqrt(stats_h[1]) * std::sqrt(stats_h[2])) {
                 order.push_back(slot);

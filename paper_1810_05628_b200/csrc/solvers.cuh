@@ -9,6 +9,7 @@
 #pragma once
 
 #include <deque>
+#include <functional>
 #include <memory>
 #include <vector>
 
@@ -68,9 +69,9 @@ struct DObj {
     int level = 0;
     double weight = 1.0;
     double eval(Counter& c, const void* z, void* grad) const;
-    // eval + (optionally) the ComplexField::isFinite test of z, read back in
-    // the same transfer as the value
-    double eval_checked(Counter& c, const void* z, void* grad, bool* nonfinite) const;
+    // charge + enqueue the evaluation and the value's copy into host_value
+    // (pinned); the caller synchronises the plan's stream
+    void eval_enqueue(Counter& c, const void* z, void* grad, double* host_value) const;
 };
 
 struct SolveOut {
@@ -80,15 +81,18 @@ struct SolveOut {
 
 // solvers.cpp:61-85; trials are formed in z_out (gradient in g_out), so the
 // accepted point needs no copy; on a stall z_out = z and g_out is scratch.
-// z_out / g_out must not alias z / dir.
+// z_out / g_out must not alias z / dir.  first_trial_hook (optional) is
+// called once, after the first trial's evaluation is enqueued and before the
+// stream is synchronised: work that assumes that trial is accepted (the
+// common case) rides on the same synchronisation.
 struct LsOut {
     double alpha = 0.0, value = 0.0;
     bool stalled = false;
-    bool nonfinite = false;   // accepted point failed isFinite (only with check_finite)
     int trials = 0;
 };
 LsOut d_linesearch(const DObj& obj, const void* z, const void* dir, Counter& ctr, int max_trials,
-                   const double* phi0, void* z_out, void* g_out, bool check_finite = false);
+                   const double* phi0, void* z_out, void* g_out,
+                   const std::function<void()>& first_trial_hook = {});
 
 // fused LBFGS kernels (lbfgs_dev.cu)
 constexpr int kMaxPairs = 64;
@@ -98,8 +102,10 @@ constexpr int kMaxPairs = 64;
 // device cannot co-schedule the grid): use the kernel-per-op path.
 bool dev_two_loop(const Plan& p, const void* const* s, const void* const* y, const double* sy, int k,
                   const void* g, void* q, double* scratch);
-// s = nz - z, y = ng - g; out_dev[0..3] = <s,y>, <s,s>, <y,y>, <ng,ng>
-// scratch: 4 x kReduceBlocks doubles + a zeroed counter
+// s = nz - z, y = ng - g; out_dev[0..4] = <s,y>, <s,s>, <y,y>, <ng,ng>,
+// count of blocks holding a non-finite nz entry.
+// scratch: kPairScratch doubles, zeroed before the first use
+constexpr int kPairScratch = 5 * kReduceBlocks + 2;
 void dev_pair_stats(const Plan& p, const void* nz, const void* z, const void* ng, const void* g, void* s_out,
                     void* y_out, double* scratch, double* out_dev);
 
