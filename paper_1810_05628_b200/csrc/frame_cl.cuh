@@ -1,0 +1,258 @@
+// frame_cl.cuh — cluster-split fused frame kernel for complex64 frames of
+// side M = 64 Q (Q = 2: M = 128, Q = 4: M = 256), w == M (patch mode).
+//
+// Same computation as frame_kernel<OP_DISTANCE/OP_INTENSITY> (frame_kernels.cuh,
+// reference objectives.cpp:59-103).  A frame of M x M complex64 (128 / 512 KiB)
+// is too large for one SM's registers or shared memory, so it is split over a
+// thread-block cluster of Q CTAs: CTA q holds frame rows [64q, 64q + 64) in
+// shared memory, and every line transform is one radix-Q butterfly stage
+// plus Q independent 64-point transforms, the latter done by the register
+// line FFT of the M = 64 kernel (frame_reg.cuh: compile-time twiddles, one
+// thread per 64-point line):
+//
+//   columns (length M, split across the cluster):
+//     forward  = DIF: radix-Q butterfly over the Q CTAs (distributed shared
+//                memory) then FFT64 over each CTA's 64 rows; frequency
+//                kr = Q k + q lands in CTA q, local row k;
+//     inverse  = DIT: FFT64 over the local rows then the radix-Q combine over
+//                the cluster, fused with the conj(P) epilogue (global stores);
+//   rows (length M, local to a CTA):
+//     forward  = DIF butterfly in shared memory then FFT64 per quarter-row,
+//                spectral operator in registers (frequency kc = Q k + p),
+//     inverse  = FFT64 of conj(R) in the same registers then the DIT combine.
+//
+// The inverse transforms use IDFT(X) = conj(DFT(conj X)) as in frame_tma.cuh,
+// and all four FFT64 passes run from one rolled loop (one copy of the body in
+// the instruction cache).  The spectral operator reads the amplitudes in the
+// frequency order it produces them: the plan keeps a copy permuted to
+// [j][q][r][p][k] = A_j[Q r + q][Q k + p] (k_perm_amp, plan.cu), so every
+// thread streams 64 contiguous floats.  Per-CTA misfit partials go to
+// misfit[j*Q + q] (fixed order, fp64).
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "frame_reg.cuh"
+
+namespace ptg {
+
+template <int Q>
+__host__ __device__ constexpr int cl_pitch() { return 64 * Q + 2; }   // complex elements per smem row
+template <int Q>
+__host__ __device__ constexpr size_t cl_smem_bytes() {
+    return sizeof(float2) * (64 * (size_t)cl_pitch<Q>() + 64 * Q);    // 64 rows + twiddle table
+}
+
+// forward DFT_Q in place, natural order
+template <int Q>
+__device__ __forceinline__ void dft_q(float2* v) {
+    if constexpr (Q == 2) dft2<false>(v[0], v[1]);
+    else dft4<false>(v[0], v[1], v[2], v[3]);
+}
+
+template <int Q, int OP, bool PROBE>
+__global__ void __launch_bounds__(64 * Q, Q == 2 ? 3 : 1)
+    frame_cl_kernel(FrameArgs<float> a, const float* __restrict__ amp_perm) {
+    namespace cg = cooperative_groups;
+    constexpr int M = 64 * Q, NT = M, PM = cl_pitch<Q>(), NPC = 64 / Q;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char cl_smem[];
+    float2* buf = reinterpret_cast<float2*>(cl_smem);   // [64][PM]: frame rows 64q..64q+63
+    float2* tw = buf + 64 * PM;                          // W_M^i, i < M
+    __shared__ double red[NT / 32];
+
+    const int q = (int)cl.block_rank();
+    const int j = a.first + (int)(blockIdx.x / Q);
+    const int t = threadIdx.x;
+    const int2 pj = a.pos[j];
+    const int n = a.n;
+    for (int i = t; i < M; i += NT) {
+        double s, c;
+        sincospi(2.0 * i / M, &s, &c);
+        tw[i] = make_float2((float)c, (float)-s);
+    }
+    float2* rb[Q];   // every CTA's frame rows (distributed shared memory)
+#pragma unroll
+    for (int s = 0; s < Q; ++s) rb[s] = cl.map_shared_rank(buf, s);
+
+    // gather psi = P o x for rows 64q + r, column t
+    {
+        const float2* zr = a.z + (size_t)(pj.x + 64 * q) * n + pj.y + t;
+        const float2* pr = a.probe + (size_t)(64 * q) * M + t;
+#pragma unroll 8
+        for (int r = 0; r < 64; ++r) {
+            float2 v = zr[(size_t)r * n];
+            if constexpr (PROBE) v = cmul(__ldg(pr + r * M), v);
+            buf[r * PM + t] = v;
+        }
+    }
+    cl.sync();
+    // column DIF butterflies: CTA q owns local rows [q NPC, (q+1) NPC) of every CTA
+#pragma unroll 2
+    for (int i = 0; i < NPC; ++i) {
+        const int r = q * NPC + i;
+        float2 v[Q];
+#pragma unroll
+        for (int s = 0; s < Q; ++s) v[s] = rb[s][r * PM + t];
+        dft_q<Q>(v);
+#pragma unroll
+        for (int s = 1; s < Q; ++s) v[s] = cmul(tw[r * s], v[s]);
+#pragma unroll
+        for (int s = 0; s < Q; ++s) rb[s][r * PM + t] = v[s];
+    }
+    cl.sync();
+
+    // row-stage roles: butterflies (row g + Q i, element m); FFT64 quarter-rows (rr, qq)
+    const int m = t % 64, g = t / 64;
+    const int rr = t % 64, qq = t / 64;
+    float2 rtw[Q];
+#pragma unroll
+    for (int s = 0; s < Q; ++s) rtw[s] = tw[m * s];
+    const float* A = amp_perm + (size_t)j * M * M + ((size_t)q * 64 + rr) * M + (size_t)qq * 64;
+    double acc = 0.0;
+    float2 x[64];
+#pragma unroll 1
+    for (int pass = 0; pass < 4; ++pass) {
+        if (pass == 0 || pass == 3) {   // column t of the local rows
+#pragma unroll
+            for (int k = 0; k < 64; ++k) x[k] = buf[k * PM + t];
+        } else if (pass == 1) {         // quarter qq of local row rr
+#pragma unroll
+            for (int c = 0; c < 64; c += 2) {
+                const float4 v = *reinterpret_cast<const float4*>(&buf[rr * PM + qq * 64 + c]);
+                x[c] = make_float2(v.x, v.y);
+                x[c + 1] = make_float2(v.z, v.w);
+            }
+        }
+        reg_fft<64, false>(x);
+        if (pass == 0) {
+#pragma unroll
+            for (int k = 0; k < 64; ++k) buf[k * PM + t] = x[k];
+            __syncthreads();
+            // row DIF butterflies (local): elements m + 64 s of rows g + Q i
+#pragma unroll 2
+            for (int i = 0; i < NPC; ++i) {
+                float2* row = buf + (g + Q * i) * PM + m;
+                float2 v[Q];
+#pragma unroll
+                for (int s = 0; s < Q; ++s) v[s] = row[64 * s];
+                dft_q<Q>(v);
+#pragma unroll
+                for (int s = 1; s < Q; ++s) v[s] = cmul(rtw[s], v[s]);
+#pragma unroll
+                for (int s = 0; s < Q; ++s) row[64 * s] = v[s];
+            }
+            __syncthreads();
+        } else if (pass == 1) {
+            // spectral operator at (kr, kc) = (Q rr + q, Q k + qq); x <- conj(R)
+            float af[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int c = 0; c < 64; c += 4) {
+                const float4 A4 = __ldg(reinterpret_cast<const float4*>(A + c));
+                const float Av[4] = {A4.x, A4.y, A4.z, A4.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float2 W = x[c + u];
+                    const float Am = Av[u];
+                    float2 R;
+                    if constexpr (OP == OP_INTENSITY) {
+                        const float r = (W.x * W.x + W.y * W.y) - Am;
+                        af[u] = fmaf(r, r, af[u]);
+                        R = make_float2(W.x * r, W.y * r);
+                    } else {
+                        // |W|^2 below the smallest normal float is treated as W = 0 (frame_tma.cuh)
+                        const float m2 = fmaf(W.x, W.x, W.y * W.y);
+                        const bool nz = m2 >= 1.17549435e-38f;
+                        const float inv = nz ? rsqrt_ftz(m2) : 0.f;
+                        const float dl = fmaf(m2, inv, -Am);
+                        af[u] = fmaf(dl, dl, af[u]);
+                        const float s = fmaf(-Am, inv, 1.f);
+                        R = make_float2(fmaf(W.x, s, nz ? 0.f : -Am), W.y * s);
+                    }
+                    x[c + u] = make_float2(R.x, -R.y);
+                }
+            }
+            acc = ((double)af[0] + (double)af[1]) + ((double)af[2] + (double)af[3]);
+        } else if (pass == 2) {
+#pragma unroll
+            for (int c = 0; c < 64; c += 2)
+                *reinterpret_cast<float4*>(&buf[rr * PM + qq * 64 + c]) = make_float4(x[c].x, x[c].y, x[c + 1].x, x[c + 1].y);
+            __syncthreads();
+            // row DIT combine (local): out[m + 64 s] = DFT_Q_s(W_M^{m p} F_p[m])
+#pragma unroll 2
+            for (int i = 0; i < NPC; ++i) {
+                float2* row = buf + (g + Q * i) * PM + m;
+                float2 v[Q];
+#pragma unroll
+                for (int s = 0; s < Q; ++s) v[s] = row[64 * s];
+#pragma unroll
+                for (int s = 1; s < Q; ++s) v[s] = cmul(rtw[s], v[s]);
+                dft_q<Q>(v);
+#pragma unroll
+                for (int s = 0; s < Q; ++s) row[64 * s] = v[s];
+            }
+            __syncthreads();
+        } else {
+#pragma unroll
+            for (int k = 0; k < 64; ++k) buf[k * PM + t] = x[k];
+        }
+    }
+
+    // per-CTA misfit partial (fixed shuffle tree + fixed warp order)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((t & 31) == 0) red[t / 32] = acc;
+    cl.sync();   // also publishes every CTA's column-transformed rows
+    if (t == 0) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < NT / 32; ++i) s += red[i];
+        a.misfit[(size_t)j * Q + q] = (OP == OP_DISTANCE) ? s / (2.0 * (double)M * (double)M) : 0.5 * s;
+    }
+
+    // column DIT combine over the cluster + epilogue: rows r + 64 s, column t
+    const float sc = (OP == OP_DISTANCE) ? 1.f / (float(M) * float(M)) : 2.f;
+    const int odd = pj.y & 1;
+    constexpr int SP = stash_pitch(M);
+#pragma unroll 2
+    for (int i = 0; i < NPC; ++i) {
+        const int r = q * NPC + i;
+        float2 v[Q];
+#pragma unroll
+        for (int s = 0; s < Q; ++s) v[s] = rb[s][r * PM + t];
+#pragma unroll
+        for (int s = 1; s < Q; ++s) v[s] = cmul(tw[r * s], v[s]);
+        dft_q<Q>(v);
+#pragma unroll
+        for (int s = 0; s < Q; ++s) {
+            const int row = r + 64 * s;
+            const float2 val = PROBE ? epi_contrib(v[s], __ldg(a.probe + (size_t)row * M + t), sc) : epi_contrib(v[s], sc);
+            if (a.planes) {
+                a.planes[(size_t)a.color[j] * n * n + (size_t)(pj.x + row) * n + pj.y + t] = val;
+            } else {
+                float2* out = a.stash + (size_t)j * M * SP + (size_t)row * SP;
+                out[odd + t] = val;
+                if (t == 0) {   // the row's two zero pads (plan.cuh stash layout)
+                    out[odd ? 0 : M] = make_float2(0.f, 0.f);
+                    out[M + 1] = make_float2(0.f, 0.f);
+                }
+            }
+        }
+    }
+    cl.sync();   // no CTA leaves while its rows may still be read remotely
+}
+
+// [j][q][r][p][k] = A_j[Q r + q][Q k + p]: amplitudes in the order the cluster
+// kernel's spectral operator consumes them
+template <int Q>
+__global__ void k_perm_amp(const float* __restrict__ in, float* __restrict__ out, size_t total) {
+    constexpr int M = 64 * Q;
+    for (size_t o = blockIdx.x * (size_t)blockDim.x + threadIdx.x; o < total; o += (size_t)gridDim.x * blockDim.x) {
+        const size_t jj = o / ((size_t)M * M);
+        const int rem = (int)(o % ((size_t)M * M));
+        const int k = rem % 64, p = (rem / 64) % Q, r = (rem / M) % 64, q = rem / (64 * M);
+        out[o] = in[jj * M * M + (size_t)(Q * r + q) * M + Q * k + p];
+    }
+}
+
+}  // namespace ptg

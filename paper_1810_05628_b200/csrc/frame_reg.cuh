@@ -81,6 +81,14 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
     return r;
 }
 
+// epilogue value sc * conj(P) * IDFT_u(R) from x = conj(IDFT_u(R)):
+// conj(P) (sc conj x), scalar FMAs with the signs in the operands
+__device__ __forceinline__ float2 epi_contrib(float2 x, float2 P, float sc) {
+    const float a = x.x * sc, b = x.y * sc;
+    return make_float2(fmaf(P.x, a, -(P.y * b)), fmaf(-P.x, b, -(P.y * a)));
+}
+__device__ __forceinline__ float2 epi_contrib(float2 x, float sc) { return make_float2(x.x * sc, -x.y * sc); }
+
 // ------------------------------------------------------ register line FFT
 // Compile-time twiddles: Taylor series evaluated by the compiler (constexpr),
 // argument reduced to [-pi, pi]; exact to ~1e-16, rounded once to fp32.

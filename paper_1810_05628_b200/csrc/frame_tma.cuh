@@ -61,14 +61,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
         : "memory");
 }
 
-// epilogue value sc * conj(P) * IDFT_u(R) from x = conj(IDFT_u(R)):
-// conj(P) (sc conj x), scalar FMAs with the signs in the operands
-__device__ __forceinline__ float2 epi_contrib(float2 x, float2 P, float sc) {
-    const float a = x.x * sc, b = x.y * sc;
-    return make_float2(fmaf(P.x, a, -(P.y * b)), fmaf(-P.x, b, -(P.y * a)));
-}
-__device__ __forceinline__ float2 epi_contrib(float2 x, float sc) { return make_float2(x.x * sc, -x.y * sc); }
-
 template <int M, int OP, bool PROBE>
 __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
     frame_tma_kernel(FrameArgs<float> a, int count, const __grid_constant__ CUtensorMap tm_z,

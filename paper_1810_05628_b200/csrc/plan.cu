@@ -17,6 +17,7 @@
 
 #include <cudaTypedefs.h>
 
+#include "frame_cl.cuh"
 #include "frame_kernels.cuh"
 #include "frame_multipass.cuh"
 #include "frame_tma.cuh"
@@ -206,12 +207,72 @@ void launch_tma(Plan& p, const FrameArgs<float>& a, int count, const void* z, co
     }
 }
 
-// objective frame kernel: TMA/register path for complex64 patch frames, smem path otherwise
+// ------------------------------------------- cluster-split frames (M = 128, 256)
+bool cl_path_ok(const Plan& p) {
+    static const bool off = getenv("PTG_NO_CLUSTER") && getenv("PTG_NO_CLUSTER")[0] == '1';   // A/B switch
+    return !off && p.prec == PTG_C64 && (p.M == 128 || p.M == 256) && p.w == p.M && p.N > 0;
+}
+
+// amplitudes (or intensities) permuted for frame_cl_kernel, rebuilt when the
+// source buffer or its contents (data_gen) change
+const float* cl_amp(Plan& p, const float* data) {
+    if (p.amp_cl_src != data || p.amp_cl_gen != p.data_gen) {
+        const size_t total = (size_t)p.N * p.MM();
+        p.amp_cl.ensure(total * sizeof(float));
+        const int grid = (int)std::min<size_t>(148 * 16, (total + 255) / 256);
+        if (p.M == 128) k_perm_amp<2><<<grid, 256, 0, p.stream>>>(data, p.amp_cl.as<float>(), total);
+        else k_perm_amp<4><<<grid, 256, 0, p.stream>>>(data, p.amp_cl.as<float>(), total);
+        PTG_CHECK_LAUNCH();
+        ++p.launches;
+        p.amp_cl_src = data;
+        p.amp_cl_gen = p.data_gen;
+    }
+    return p.amp_cl.as<const float>();
+}
+
+template <int Q, int OP, bool PROBE>
+void launch_cl_t(Plan& p, const FrameArgs<float>& a, int count, const float* amp_perm) {
+    constexpr size_t smem = cl_smem_bytes<Q>();
+    auto kern = frame_cl_kernel<Q, OP, PROBE>;
+    static bool attr = false;
+    if (!attr) {
+        PTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)count * Q);
+    cfg.blockDim = dim3(64 * Q);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = p.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = Q;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PTG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, amp_perm));
+}
+
+template <int OP>
+void launch_cl(Plan& p, const FrameArgs<float>& a, int count, const float* data) {
+    const float* ap = cl_amp(p, data);
+    const bool pr = a.probe != nullptr;
+    if (p.M == 128) pr ? launch_cl_t<2, OP, true>(p, a, count, ap) : launch_cl_t<2, OP, false>(p, a, count, ap);
+    else pr ? launch_cl_t<4, OP, true>(p, a, count, ap) : launch_cl_t<4, OP, false>(p, a, count, ap);
+}
+
+// objective frame kernel: TMA/register path for complex64 patch frames up to
+// M = 64, cluster-split register path for M = 128 / 256, smem path otherwise
 template <typename T, int OP>
 void launch_objective(Plan& p, const FrameArgs<T>& a, int count, const void* z, const T* data) {
     if constexpr (sizeof(T) == 4) {
         if (tma_path_ok(p)) {
             launch_tma<OP>(p, a, count, z, data);
+            return;
+        }
+        if (p.cl) {
+            launch_cl<OP>(p, a, count, data);
             return;
         }
     }
@@ -685,6 +746,7 @@ void build_chunks(Plan& p) {
     p.tiles_x = (p.n + kTileW - 1) / kTileW;
     p.tiles_y = (p.n + kTileH - 1) / kTileH;
     p.mp = !frame_single_cta(p.prec, p.M);
+    p.cl = cl_path_ok(p);
     p.planes_mode = choose_planes(p);
     if (p.planes_mode) {   // one chunk, no tile lists, no stash
         auto c = std::make_unique<Chunk>();
@@ -694,8 +756,8 @@ void build_chunks(Plan& p) {
         p.chunks.clear();
         p.chunks.push_back(std::move(c));
         p.stash.alloc(p.celem());
-        p.misfit_per_pos = 1;
-        p.misfit.alloc(std::max<size_t>(1, (size_t)p.N) * sizeof(double));
+        p.misfit_per_pos = p.cl ? p.M / 64 : 1;
+        p.misfit.alloc(std::max<size_t>(1, (size_t)p.N * p.misfit_per_pos) * sizeof(double));
         p.dotp.alloc((size_t)kPlaneBlocks * sizeof(double));
         return;
     }
@@ -755,7 +817,7 @@ void build_chunks(Plan& p) {
         p.chunks.push_back(std::move(c));
     }
     p.stash.alloc(std::max<size_t>(1, (size_t)cs * p.w * stash_pitch(p.w)) * p.celem());
-    p.misfit_per_pos = p.mp ? p.M / kMpLines : 1;
+    p.misfit_per_pos = p.cl ? p.M / 64 : p.mp ? p.M / kMpLines : 1;
     if (p.mp) {   // ~64 MiB of whole-frame scratch: stays L2-resident between passes
         const size_t fb = p.MM() * p.celem();
         p.mp_chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(p.N, 1), ((size_t)64 << 20) / fb));
@@ -863,6 +925,7 @@ static void validate_and_amp(Plan& p) {
     }
     p.amp_valid = true;
     p.inten_valid = true;
+    ++p.data_gen;
 }
 
 void plan_set_data_device(Plan& p, const void* data, int dtype) {
@@ -899,6 +962,7 @@ void plan_ensure(Plan& p, int metric) {
             ++p.launches;
         }
         p.inten_valid = true;
+        ++p.data_gen;
     }
     if (metric == PTG_DISTANCE && !p.amp_valid) {
         if (!p.inten_valid) raise(PTG_ERR_CONFIG, "plan has no diffraction data");
@@ -926,7 +990,7 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
             // frame_kernel writes stash[j*w*w]; offset the base so j - first maps to 0
             a.stash = reinterpret_cast<C*>(p.stash.as<C>()) - (size_t)c.first * p.w * stash_pitch(p.w);
             p.ev_begin(0);
-            if (p.mp) {
+            if (p.mp && !p.cl) {
                 if (metric == PTG_DISTANCE) launch_mp<T, OP_DISTANCE>(p, a, c.first, c.count);
                 else launch_mp<T, OP_INTENSITY>(p, a, c.first, c.count);
             } else {
@@ -951,8 +1015,8 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
             p.ev_begin(1);
             PTG_CUDA(cudaLaunchKernelEx(&cfg, k_plane_reduce<T>, p.planes.as<const C>(), p.ncolors, p.nn(),
                                         static_cast<const C*>(v), static_cast<const C*>(z), static_cast<C*>(grad),
-                                        p.dotp.as<double>(), p.misfit.as<const double>(), p.N, value_dev,
-                                        p.counter.as<unsigned int>()));
+                                        p.dotp.as<double>(), p.misfit.as<const double>(), p.N * p.misfit_per_pos,
+                                        value_dev, p.counter.as<unsigned int>()));
             p.ev_end();
             ++p.launches;
             return;

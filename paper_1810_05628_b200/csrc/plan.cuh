@@ -112,6 +112,15 @@ struct Plan {
     std::vector<int> color_h;
     DevMem color, planes;
 
+    // cluster-split objective kernel for complex64 M = 128 / 256 (frame_cl.cuh):
+    // amplitudes permuted into its frequency order, rebuilt when the source
+    // buffer or the data generation changes
+    bool cl = false;
+    DevMem amp_cl;
+    const void* amp_cl_src = nullptr;
+    uint64_t amp_cl_gen = ~0ull;
+    uint64_t data_gen = 0;   // bumped whenever amp / inten are rewritten
+
     // multi-pass path for frames larger than one CTA (frame_multipass.cuh)
     bool mp = false;
     int mp_chunk = 0;                // positions per scratch sub-chunk
