@@ -38,9 +38,16 @@ namespace ptg {
 
 template <int Q>
 __host__ __device__ constexpr int cl_pitch() { return 64 * Q + 2; }   // complex elements per smem row
+// Q = 4 stages the CTA's 64 amplitude rows in shared memory by TMA bulk copies
+// issued at kernel start (pitch M + 4 floats: conflict-free 128-bit reads)
+template <int Q>
+__host__ __device__ constexpr bool cl_amp_staged() { return Q == 4; }
+template <int Q>
+__host__ __device__ constexpr int cl_amp_pitch() { return 64 * Q + 4; }
 template <int Q>
 __host__ __device__ constexpr size_t cl_smem_bytes() {
-    return sizeof(float2) * (64 * (size_t)cl_pitch<Q>() + 64 * Q);    // 64 rows + twiddle table
+    return sizeof(float2) * (64 * (size_t)cl_pitch<Q>() + 64 * Q)     // 64 rows + twiddle table
+           + (cl_amp_staged<Q>() ? sizeof(float) * 64 * (size_t)cl_amp_pitch<Q>() : 0);
 }
 
 // forward DFT_Q in place, natural order
@@ -51,7 +58,7 @@ __device__ __forceinline__ void dft_q(float2* v) {
 }
 
 template <int Q, int OP, bool PROBE>
-__global__ void __launch_bounds__(64 * Q, Q == 2 ? 3 : 1)
+__global__ void __launch_bounds__(64 * Q, Q == 2 ? 2 : 1)
     frame_cl_kernel(FrameArgs<float> a, const float* __restrict__ amp_perm) {
     namespace cg = cooperative_groups;
     constexpr int M = 64 * Q, NT = M, PM = cl_pitch<Q>(), NPC = 64 / Q;
@@ -66,39 +73,67 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 3 : 1)
     const int t = threadIdx.x;
     const int2 pj = a.pos[j];
     const int n = a.n;
+    // cluster start handshake, split: the wait sits before the first remote store
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    float* amp_s = reinterpret_cast<float*>(tw + M);   // [64][M + 4] (Q = 4)
+    __shared__ __align__(8) unsigned long long bar_a;
+    if constexpr (cl_amp_staged<Q>()) {
+        if (t == 0) {
+            mbar_init(&bar_a, 1);
+            fence_mbarrier_init();
+        }
+        __syncthreads();
+        if (t < 32) {   // this CTA's 64 permuted amplitude rows, one bulk copy per row
+            const float* src = amp_perm + (size_t)j * M * M + (size_t)q * 64 * M;
+            if (t == 0) mbar_arrive_expect_tx(&bar_a, 64 * M * sizeof(float));
+            __syncwarp();
+            for (int r = t; r < 64; r += 32)
+                tma_bulk_g2s(amp_s + r * cl_amp_pitch<Q>(), src + (size_t)r * M, M * sizeof(float), &bar_a);
+        }
+    }
     for (int i = t; i < M; i += NT) {
-        double s, c;
-        sincospi(2.0 * i / M, &s, &c);
-        tw[i] = make_float2((float)c, (float)-s);
+        double sn, cs;
+        sincospi(2.0 * i / M, &sn, &cs);
+        tw[i] = make_float2((float)cs, (float)-sn);
     }
     float2* rb[Q];   // every CTA's frame rows (distributed shared memory)
 #pragma unroll
     for (int s = 0; s < Q; ++s) rb[s] = cl.map_shared_rank(buf, s);
 
-    // gather psi = P o x for rows 64q + r, column t
+    // gather fused with the column DIF butterflies: CTA q forms butterfly rows
+    // r = q NPC + i (window rows r + 64 s, column t) straight from global memory
+    // and stores output s into CTA s's row r
+    float2 x[64];
+    __syncthreads();                                              // twiddle table
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");   // every CTA of the cluster runs
     {
-        const float2* zr = a.z + (size_t)(pj.x + 64 * q) * n + pj.y + t;
-        const float2* pr = a.probe + (size_t)(64 * q) * M + t;
-#pragma unroll 8
-        for (int r = 0; r < 64; ++r) {
-            float2 v = zr[(size_t)r * n];
-            if constexpr (PROBE) v = cmul(__ldg(pr + r * M), v);
-            buf[r * PM + t] = v;
+        // batches of BT butterflies: their Q z values and probe values in flight together
+        constexpr int BT = 16 / Q;
+        const float2* zc = a.z + (size_t)pj.x * n + pj.y + t;
+#pragma unroll 1
+        for (int b = 0; b < NPC; b += BT) {
+            float2 zv[BT * Q], pv[BT * Q];
+#pragma unroll
+            for (int i = 0; i < BT; ++i)
+#pragma unroll
+                for (int s = 0; s < Q; ++s) {
+                    const int row = q * NPC + b + i + 64 * s;
+                    zv[i * Q + s] = zc[(size_t)row * n];
+                    if constexpr (PROBE) pv[i * Q + s] = __ldg(a.probe + (size_t)row * M + t);
+                }
+#pragma unroll
+            for (int i = 0; i < BT; ++i) {
+                const int r = q * NPC + b + i;
+                float2 v[Q];
+#pragma unroll
+                for (int s = 0; s < Q; ++s) v[s] = PROBE ? cmul(pv[i * Q + s], zv[i * Q + s]) : zv[i * Q + s];
+                dft_q<Q>(v);
+#pragma unroll
+                for (int s = 1; s < Q; ++s) v[s] = cmul(tw[r * s], v[s]);
+#pragma unroll
+                for (int s = 0; s < Q; ++s) rb[s][r * PM + t] = v[s];
+            }
         }
-    }
-    cl.sync();
-    // column DIF butterflies: CTA q owns local rows [q NPC, (q+1) NPC) of every CTA
-#pragma unroll 2
-    for (int i = 0; i < NPC; ++i) {
-        const int r = q * NPC + i;
-        float2 v[Q];
-#pragma unroll
-        for (int s = 0; s < Q; ++s) v[s] = rb[s][r * PM + t];
-        dft_q<Q>(v);
-#pragma unroll
-        for (int s = 1; s < Q; ++s) v[s] = cmul(tw[r * s], v[s]);
-#pragma unroll
-        for (int s = 0; s < Q; ++s) rb[s][r * PM + t] = v[s];
     }
     cl.sync();
 
@@ -110,7 +145,6 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 3 : 1)
     for (int s = 0; s < Q; ++s) rtw[s] = tw[m * s];
     const float* A = amp_perm + (size_t)j * M * M + ((size_t)q * 64 + rr) * M + (size_t)qq * 64;
     double acc = 0.0;
-    float2 x[64];
 #pragma unroll 1
     for (int pass = 0; pass < 4; ++pass) {
         if (pass == 0 || pass == 3) {   // column t of the local rows
@@ -146,9 +180,12 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 3 : 1)
         } else if (pass == 1) {
             // spectral operator at (kr, kc) = (Q rr + q, Q k + qq); x <- conj(R)
             float af[4] = {0.f, 0.f, 0.f, 0.f};
+            if constexpr (cl_amp_staged<Q>()) mbar_wait(&bar_a, 0);
 #pragma unroll
             for (int c = 0; c < 64; c += 4) {
-                const float4 A4 = __ldg(reinterpret_cast<const float4*>(A + c));
+                const float4 A4 = cl_amp_staged<Q>()
+                                      ? *reinterpret_cast<const float4*>(amp_s + rr * cl_amp_pitch<Q>() + qq * 64 + c)
+                                      : __ldg(reinterpret_cast<const float4*>(A + c));
                 const float Av[4] = {A4.x, A4.y, A4.z, A4.w};
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
@@ -197,6 +234,13 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 3 : 1)
             for (int k = 0; k < 64; ++k) buf[k * PM + t] = x[k];
         }
     }
+    // epilogue probe values (rows q NPC + i + 64 s, column t) in flight across the barrier
+    if constexpr (PROBE) {
+#pragma unroll
+        for (int i = 0; i < NPC; ++i)
+#pragma unroll
+            for (int s = 0; s < Q; ++s) x[i * Q + s] = __ldg(a.probe + (size_t)(q * NPC + i + 64 * s) * M + t);
+    }
 
     // per-CTA misfit partial (fixed shuffle tree + fixed warp order)
 #pragma unroll
@@ -214,7 +258,7 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 3 : 1)
     const float sc = (OP == OP_DISTANCE) ? 1.f / (float(M) * float(M)) : 2.f;
     const int odd = pj.y & 1;
     constexpr int SP = stash_pitch(M);
-#pragma unroll 2
+#pragma unroll   // x[] is indexed by i: full unroll keeps it in registers
     for (int i = 0; i < NPC; ++i) {
         const int r = q * NPC + i;
         float2 v[Q];
@@ -226,7 +270,7 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 3 : 1)
 #pragma unroll
         for (int s = 0; s < Q; ++s) {
             const int row = r + 64 * s;
-            const float2 val = PROBE ? epi_contrib(v[s], __ldg(a.probe + (size_t)row * M + t), sc) : epi_contrib(v[s], sc);
+            const float2 val = PROBE ? epi_contrib(v[s], x[i * Q + s], sc) : epi_contrib(v[s], sc);
             if (a.planes) {
                 a.planes[(size_t)a.color[j] * n * n + (size_t)(pj.x + row) * n + pj.y + t] = val;
             } else {
