@@ -1,33 +1,34 @@
 // frame_cl.cuh — cluster-split fused frame kernel for complex64 frames of
-// side M = 64 Q (Q = 2: M = 128, Q = 4: M = 256), w == M (patch mode).
+// side M = Q L (M = 128, 256; local line L = 32 or 64), w == M (patch mode).
 //
 // Same computation as frame_kernel<OP_DISTANCE/OP_INTENSITY> (frame_kernels.cuh,
 // reference objectives.cpp:59-103).  A frame of M x M complex64 (128 / 512 KiB)
 // is too large for one SM's registers or shared memory, so it is split over a
-// thread-block cluster of Q CTAs: CTA q holds frame rows [64q, 64q + 64) in
+// thread-block cluster of Q CTAs: CTA q holds frame rows [Lq, Lq + L) in
 // shared memory, and every line transform is one radix-Q butterfly stage
-// plus Q independent 64-point transforms, the latter done by the register
+// plus Q independent L-point transforms, the latter done by the register
 // line FFT of the M = 64 kernel (frame_reg.cuh: compile-time twiddles, one
-// thread per 64-point line):
+// thread per L-point line):
 //
 //   columns (length M, split across the cluster):
 //     forward  = DIF: radix-Q butterfly over the Q CTAs (distributed shared
-//                memory) then FFT64 over each CTA's 64 rows; frequency
+//                memory) then FFT_L over each CTA's L rows; frequency
 //                kr = Q k + q lands in CTA q, local row k;
-//     inverse  = DIT: FFT64 over the local rows then the radix-Q combine over
-//                the cluster, fused with the conj(P) epilogue (global stores);
+//     inverse  = DIT: FFT_L over the local rows, pushed to the CTA owning the
+//                output rows, then the radix-Q combine fused with the conj(P)
+//                epilogue (global stores);
 //   rows (length M, local to a CTA):
-//     forward  = DIF butterfly in shared memory then FFT64 per quarter-row,
+//     forward  = DIF butterfly in shared memory then FFT_L per row part,
 //                spectral operator in registers (frequency kc = Q k + p),
-//     inverse  = FFT64 of conj(R) in the same registers then the DIT combine.
+//     inverse  = FFT_L of conj(R) in the same registers then the DIT combine.
 //
 // The inverse transforms use IDFT(X) = conj(DFT(conj X)) as in frame_tma.cuh,
-// and all four FFT64 passes run from one rolled loop (one copy of the body in
+// and all four FFT_L passes run from one rolled loop (one copy of the body in
 // the instruction cache).  The spectral operator reads the amplitudes in the
 // frequency order it produces them: the plan keeps a copy permuted to
 // [j][q][r][p][k] = A_j[Q r + q][Q k + p] (k_perm_amp, plan.cu), so every
-// thread streams 64 contiguous floats.  Per-CTA misfit partials go to
-// misfit[j*Q + q] (fixed order, fp64).
+// thread streams L contiguous floats.  Per-CTA misfit partials go to
+// misfit[j*M/32 + q] (fixed order, fp64).
 #pragma once
 
 #include <cooperative_groups.h>
@@ -36,36 +37,40 @@
 
 namespace ptg {
 
-template <int Q>
-__host__ __device__ constexpr int cl_pitch() { return 64 * Q + 2; }   // complex elements per smem row
-// Q = 4 stages the CTA's 64 amplitude rows in shared memory by TMA bulk copies
-// issued at kernel start (pitch M + 4 floats: conflict-free 128-bit reads)
-template <int Q>
-__host__ __device__ constexpr bool cl_amp_staged() { return Q == 4; }
-template <int Q>
-__host__ __device__ constexpr int cl_amp_pitch() { return 64 * Q + 4; }
-template <int Q>
+// Q CTAs x L local rows, M = Q L.  The CTA's L amplitude rows are staged in
+// shared memory by TMA bulk copies issued at kernel start (pitch M + 4
+// floats: conflict-free 128-bit reads) when they fit next to the frame rows.
+template <int Q, int L>
+__host__ __device__ constexpr int cl_pitch() { return Q * L + 2; }   // complex elements per smem row
+template <int Q, int L>
+__host__ __device__ constexpr bool cl_amp_staged() { return !(Q == 2 && L == 64); }
+template <int Q, int L>
+__host__ __device__ constexpr int cl_amp_pitch() { return Q * L + 4; }
+template <int Q, int L>
 __host__ __device__ constexpr size_t cl_smem_bytes() {
-    return sizeof(float2) * (64 * (size_t)cl_pitch<Q>() + 64 * Q)     // 64 rows + twiddle table
-           + (cl_amp_staged<Q>() ? sizeof(float) * 64 * (size_t)cl_amp_pitch<Q>() : 0);
+    return sizeof(float2) * ((size_t)L * cl_pitch<Q, L>() + (size_t)Q * L)     // L rows + twiddle table
+           + (cl_amp_staged<Q, L>() ? sizeof(float) * (size_t)L * cl_amp_pitch<Q, L>() : 0);
 }
+template <int Q, int L>
+__host__ __device__ constexpr int cl_min_blocks() { return L == 32 ? (Q == 4 ? 4 : 2) : Q == 2 ? 2 : 1; }
 
 // forward DFT_Q in place, natural order
 template <int Q>
 __device__ __forceinline__ void dft_q(float2* v) {
     if constexpr (Q == 2) dft2<false>(v[0], v[1]);
-    else dft4<false>(v[0], v[1], v[2], v[3]);
+    else if constexpr (Q == 4) dft4<false>(v[0], v[1], v[2], v[3]);
+    else dft8<false>(v);
 }
 
-template <int Q, int OP, bool PROBE>
-__global__ void __launch_bounds__(64 * Q, Q == 2 ? 2 : 1)
-    frame_cl_kernel(FrameArgs<float> a, const float* __restrict__ amp_perm) {
+template <int Q, int L, int OP, bool PROBE>
+__global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
+    frame_cl_kernel(FrameArgs<float> a, const float* __restrict__ amp_perm, const float2* __restrict__ tw_g) {
     namespace cg = cooperative_groups;
-    constexpr int M = 64 * Q, NT = M, PM = cl_pitch<Q>(), NPC = 64 / Q;
+    constexpr int M = Q * L, NT = M, PM = cl_pitch<Q, L>(), NPC = L / Q, AP = cl_amp_pitch<Q, L>();
     cg::cluster_group cl = cg::this_cluster();
     extern __shared__ __align__(16) unsigned char cl_smem[];
-    float2* buf = reinterpret_cast<float2*>(cl_smem);   // [64][PM]: frame rows 64q..64q+63
-    float2* tw = buf + 64 * PM;                          // W_M^i, i < M
+    float2* buf = reinterpret_cast<float2*>(cl_smem);   // [L][PM]: frame rows Lq..Lq+L-1
+    float2* tw = buf + L * PM;                           // W_M^i, i < M
     __shared__ double red[NT / 32];
 
     const int q = (int)cl.block_rank();
@@ -75,27 +80,23 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 2 : 1)
     const int n = a.n;
     // cluster start handshake, split: the wait sits before the first remote store
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-    float* amp_s = reinterpret_cast<float*>(tw + M);   // [64][M + 4] (Q = 4)
+    float* amp_s = reinterpret_cast<float*>(tw + M);   // [L][M + 4] (staged variants)
     __shared__ __align__(8) unsigned long long bar_a;
-    if constexpr (cl_amp_staged<Q>()) {
+    if constexpr (cl_amp_staged<Q, L>()) {
         if (t == 0) {
             mbar_init(&bar_a, 1);
             fence_mbarrier_init();
         }
         __syncthreads();
-        if (t < 32) {   // this CTA's 64 permuted amplitude rows, one bulk copy per row
-            const float* src = amp_perm + (size_t)j * M * M + (size_t)q * 64 * M;
-            if (t == 0) mbar_arrive_expect_tx(&bar_a, 64 * M * sizeof(float));
+        if (t < 32) {   // this CTA's L permuted amplitude rows, one bulk copy per row
+            const float* src = amp_perm + (size_t)j * M * M + (size_t)q * L * M;
+            if (t == 0) mbar_arrive_expect_tx(&bar_a, L * M * sizeof(float));
             __syncwarp();
-            for (int r = t; r < 64; r += 32)
-                tma_bulk_g2s(amp_s + r * cl_amp_pitch<Q>(), src + (size_t)r * M, M * sizeof(float), &bar_a);
+            for (int r = t; r < L; r += 32)
+                tma_bulk_g2s(amp_s + r * AP, src + (size_t)r * M, M * sizeof(float), &bar_a);
         }
     }
-    for (int i = t; i < M; i += NT) {
-        double sn, cs;
-        sincospi(2.0 * i / M, &sn, &cs);
-        tw[i] = make_float2((float)cs, (float)-sn);
-    }
+    for (int i = t; i < M; i += NT) tw[i] = __ldg(tw_g + i);   // W_M^i (host fp64, rounded once)
     float2* rb[Q];   // every CTA's frame rows (distributed shared memory)
 #pragma unroll
     for (int s = 0; s < Q; ++s) rb[s] = cl.map_shared_rank(buf, s);
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 2 : 1)
     // gather fused with the column DIF butterflies: CTA q forms butterfly rows
     // r = q NPC + i (window rows r + 64 s, column t) straight from global memory
     // and stores output s into CTA s's row r
-    float2 x[64];
+    float2 x[L];
     __syncthreads();                                              // twiddle table
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");   // every CTA of the cluster runs
     {
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 2 : 1)
             for (int i = 0; i < BT; ++i)
 #pragma unroll
                 for (int s = 0; s < Q; ++s) {
-                    const int row = q * NPC + b + i + 64 * s;
+                    const int row = q * NPC + b + i + L * s;
                     zv[i * Q + s] = zc[(size_t)row * n];
                     if constexpr (PROBE) pv[i * Q + s] = __ldg(a.probe + (size_t)row * M + t);
                 }
@@ -138,30 +139,32 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 2 : 1)
     cl.sync();
 
     // row-stage roles: butterflies (row g + Q i, element m); FFT64 quarter-rows (rr, qq)
-    const int m = t % 64, g = t / 64;
-    const int rr = t % 64, qq = t / 64;
+    const int m = t % L, g = t / L;
+    const int rr = t % L, qq = t / L;
     float2 rtw[Q];
 #pragma unroll
     for (int s = 0; s < Q; ++s) rtw[s] = tw[m * s];
-    const float* A = amp_perm + (size_t)j * M * M + ((size_t)q * 64 + rr) * M + (size_t)qq * 64;
+    const float* A = amp_perm + (size_t)j * M * M + ((size_t)q * L + rr) * M + (size_t)qq * L;
     double acc = 0.0;
 #pragma unroll 1
     for (int pass = 0; pass < 4; ++pass) {
         if (pass == 0 || pass == 3) {   // column t of the local rows
 #pragma unroll
-            for (int k = 0; k < 64; ++k) x[k] = buf[k * PM + t];
+            for (int k = 0; k < L; ++k) x[k] = buf[k * PM + t];
+            // pass 3: this CTA's rows are consumed; the other CTAs may push into them
+            if (pass == 3) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         } else if (pass == 1) {         // quarter qq of local row rr
 #pragma unroll
-            for (int c = 0; c < 64; c += 2) {
-                const float4 v = *reinterpret_cast<const float4*>(&buf[rr * PM + qq * 64 + c]);
+            for (int c = 0; c < L; c += 2) {
+                const float4 v = *reinterpret_cast<const float4*>(&buf[rr * PM + qq * L + c]);
                 x[c] = make_float2(v.x, v.y);
                 x[c + 1] = make_float2(v.z, v.w);
             }
         }
-        reg_fft<64, false>(x);
+        reg_fft<L, false>(x);
         if (pass == 0) {
 #pragma unroll
-            for (int k = 0; k < 64; ++k) buf[k * PM + t] = x[k];
+            for (int k = 0; k < L; ++k) buf[k * PM + t] = x[k];
             __syncthreads();
             // row DIF butterflies (local): elements m + 64 s of rows g + Q i
 #pragma unroll 2
@@ -169,22 +172,22 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 2 : 1)
                 float2* row = buf + (g + Q * i) * PM + m;
                 float2 v[Q];
 #pragma unroll
-                for (int s = 0; s < Q; ++s) v[s] = row[64 * s];
+                for (int s = 0; s < Q; ++s) v[s] = row[L * s];
                 dft_q<Q>(v);
 #pragma unroll
                 for (int s = 1; s < Q; ++s) v[s] = cmul(rtw[s], v[s]);
 #pragma unroll
-                for (int s = 0; s < Q; ++s) row[64 * s] = v[s];
+                for (int s = 0; s < Q; ++s) row[L * s] = v[s];
             }
             __syncthreads();
         } else if (pass == 1) {
             // spectral operator at (kr, kc) = (Q rr + q, Q k + qq); x <- conj(R)
             float af[4] = {0.f, 0.f, 0.f, 0.f};
-            if constexpr (cl_amp_staged<Q>()) mbar_wait(&bar_a, 0);
+            if constexpr (cl_amp_staged<Q, L>()) mbar_wait(&bar_a, 0);
 #pragma unroll
-            for (int c = 0; c < 64; c += 4) {
-                const float4 A4 = cl_amp_staged<Q>()
-                                      ? *reinterpret_cast<const float4*>(amp_s + rr * cl_amp_pitch<Q>() + qq * 64 + c)
+            for (int c = 0; c < L; c += 4) {
+                const float4 A4 = cl_amp_staged<Q, L>()
+                                      ? *reinterpret_cast<const float4*>(amp_s + rr * AP + qq * L + c)
                                       : __ldg(reinterpret_cast<const float4*>(A + c));
                 const float Av[4] = {A4.x, A4.y, A4.z, A4.w};
 #pragma unroll
@@ -212,8 +215,8 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 2 : 1)
             acc = ((double)af[0] + (double)af[1]) + ((double)af[2] + (double)af[3]);
         } else if (pass == 2) {
 #pragma unroll
-            for (int c = 0; c < 64; c += 2)
-                *reinterpret_cast<float4*>(&buf[rr * PM + qq * 64 + c]) = make_float4(x[c].x, x[c].y, x[c + 1].x, x[c + 1].y);
+            for (int c = 0; c < L; c += 2)
+                *reinterpret_cast<float4*>(&buf[rr * PM + qq * L + c]) = make_float4(x[c].x, x[c].y, x[c + 1].x, x[c + 1].y);
             __syncthreads();
             // row DIT combine (local): out[m + 64 s] = DFT_Q_s(W_M^{m p} F_p[m])
 #pragma unroll 2
@@ -221,17 +224,20 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 2 : 1)
                 float2* row = buf + (g + Q * i) * PM + m;
                 float2 v[Q];
 #pragma unroll
-                for (int s = 0; s < Q; ++s) v[s] = row[64 * s];
+                for (int s = 0; s < Q; ++s) v[s] = row[L * s];
 #pragma unroll
                 for (int s = 1; s < Q; ++s) v[s] = cmul(rtw[s], v[s]);
                 dft_q<Q>(v);
 #pragma unroll
-                for (int s = 0; s < Q; ++s) row[64 * s] = v[s];
+                for (int s = 0; s < Q; ++s) row[L * s] = v[s];
             }
             __syncthreads();
         } else {
+            // push G_q[m] (column t) to the CTA that combines row m: its local row
+            // (m % NPC) Q + q, so the combine reads only local shared memory
+            asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 #pragma unroll
-            for (int k = 0; k < 64; ++k) buf[k * PM + t] = x[k];
+            for (int k = 0; k < L; ++k) rb[k / NPC][((k % NPC) * Q + q) * PM + t] = x[k];
         }
     }
     // epilogue probe values (rows q NPC + i + 64 s, column t) in flight across the barrier
@@ -239,19 +245,22 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 2 : 1)
 #pragma unroll
         for (int i = 0; i < NPC; ++i)
 #pragma unroll
-            for (int s = 0; s < Q; ++s) x[i * Q + s] = __ldg(a.probe + (size_t)(q * NPC + i + 64 * s) * M + t);
+            for (int s = 0; s < Q; ++s) x[i * Q + s] = __ldg(a.probe + (size_t)(q * NPC + i + L * s) * M + t);
     }
 
     // per-CTA misfit partial (fixed shuffle tree + fixed warp order)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((t & 31) == 0) red[t / 32] = acc;
-    cl.sync();   // also publishes every CTA's column-transformed rows
+    cl.sync();   // every push has landed; no remote access after this point
     if (t == 0) {
         double s = 0.0;
 #pragma unroll
         for (int i = 0; i < NT / 32; ++i) s += red[i];
-        a.misfit[(size_t)j * Q + q] = (OP == OP_DISTANCE) ? s / (2.0 * (double)M * (double)M) : 0.5 * s;
+        // misfit slots per position: M / 32 (the plan's layout for either split)
+        constexpr int MPP = M / 32;
+        a.misfit[(size_t)j * MPP + q] = (OP == OP_DISTANCE) ? s / (2.0 * (double)M * (double)M) : 0.5 * s;
+        if constexpr (MPP > Q) a.misfit[(size_t)j * MPP + Q + q] = 0.0;
     }
 
     // column DIT combine over the cluster + epilogue: rows r + 64 s, column t
@@ -263,13 +272,13 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 2 : 1)
         const int r = q * NPC + i;
         float2 v[Q];
 #pragma unroll
-        for (int s = 0; s < Q; ++s) v[s] = rb[s][r * PM + t];
+        for (int s = 0; s < Q; ++s) v[s] = buf[(i * Q + s) * PM + t];   // G_s[r], pushed by CTA s
 #pragma unroll
         for (int s = 1; s < Q; ++s) v[s] = cmul(tw[r * s], v[s]);
         dft_q<Q>(v);
 #pragma unroll
         for (int s = 0; s < Q; ++s) {
-            const int row = r + 64 * s;
+            const int row = r + L * s;
             const float2 val = PROBE ? epi_contrib(v[s], x[i * Q + s], sc) : epi_contrib(v[s], sc);
             if (a.planes) {
                 a.planes[(size_t)a.color[j] * n * n + (size_t)(pj.x + row) * n + pj.y + t] = val;
@@ -283,18 +292,17 @@ __global__ void __launch_bounds__(64 * Q, Q == 2 ? 2 : 1)
             }
         }
     }
-    cl.sync();   // no CTA leaves while its rows may still be read remotely
 }
 
 // [j][q][r][p][k] = A_j[Q r + q][Q k + p]: amplitudes in the order the cluster
 // kernel's spectral operator consumes them
-template <int Q>
+template <int Q, int L>
 __global__ void k_perm_amp(const float* __restrict__ in, float* __restrict__ out, size_t total) {
-    constexpr int M = 64 * Q;
+    constexpr int M = Q * L;
     for (size_t o = blockIdx.x * (size_t)blockDim.x + threadIdx.x; o < total; o += (size_t)gridDim.x * blockDim.x) {
         const size_t jj = o / ((size_t)M * M);
         const int rem = (int)(o % ((size_t)M * M));
-        const int k = rem % 64, p = (rem / 64) % Q, r = (rem / M) % 64, q = rem / (64 * M);
+        const int k = rem % L, p = (rem / L) % Q, r = (rem / M) % L, q = rem / (L * M);
         out[o] = in[jj * M * M + (size_t)(Q * r + q) * M + Q * k + p];
     }
 }

@@ -213,27 +213,41 @@ bool cl_path_ok(const Plan& p) {
     return !off && p.prec == PTG_C64 && (p.M == 128 || p.M == 256) && p.w == p.M && p.N > 0;
 }
 
+// local line length of the cluster kernel: M = Q L with L = 32 (default:
+// twice the CTAs per SM) or 64 (PTG_CL_L=64, A/B)
+int cl_line(const Plan& p) {
+    static const int env = getenv("PTG_CL_L") ? atoi(getenv("PTG_CL_L")) : 0;
+    return env == 64 ? 64 : 32;
+}
+
+template <int Q, int L>
+void perm_amp(Plan& p, const float* data, size_t total) {
+    const int grid = (int)std::min<size_t>(148 * 16, (total + 255) / 256);
+    k_perm_amp<Q, L><<<grid, 256, 0, p.stream>>>(data, p.amp_cl.as<float>(), total);
+    PTG_CHECK_LAUNCH();
+    ++p.launches;
+}
+
 // amplitudes (or intensities) permuted for frame_cl_kernel, rebuilt when the
-// source buffer or its contents (data_gen) change
+// source buffer, its contents (data_gen) or the split change
 const float* cl_amp(Plan& p, const float* data) {
-    if (p.amp_cl_src != data || p.amp_cl_gen != p.data_gen) {
+    const int L = cl_line(p);
+    if (p.amp_cl_src != data || p.amp_cl_gen != p.data_gen || p.amp_cl_line != L) {
         const size_t total = (size_t)p.N * p.MM();
         p.amp_cl.ensure(total * sizeof(float));
-        const int grid = (int)std::min<size_t>(148 * 16, (total + 255) / 256);
-        if (p.M == 128) k_perm_amp<2><<<grid, 256, 0, p.stream>>>(data, p.amp_cl.as<float>(), total);
-        else k_perm_amp<4><<<grid, 256, 0, p.stream>>>(data, p.amp_cl.as<float>(), total);
-        PTG_CHECK_LAUNCH();
-        ++p.launches;
+        if (p.M == 128) L == 32 ? perm_amp<4, 32>(p, data, total) : perm_amp<2, 64>(p, data, total);
+        else L == 32 ? perm_amp<8, 32>(p, data, total) : perm_amp<4, 64>(p, data, total);
         p.amp_cl_src = data;
         p.amp_cl_gen = p.data_gen;
+        p.amp_cl_line = L;
     }
     return p.amp_cl.as<const float>();
 }
 
-template <int Q, int OP, bool PROBE>
-void launch_cl_t(Plan& p, const FrameArgs<float>& a, int count, const float* amp_perm) {
-    constexpr size_t smem = cl_smem_bytes<Q>();
-    auto kern = frame_cl_kernel<Q, OP, PROBE>;
+template <int Q, int L, int OP, bool PROBE>
+void launch_cl_t(Plan& p, const FrameArgs<float>& a, int count, const float* amp_perm, const float2* tw) {
+    constexpr size_t smem = cl_smem_bytes<Q, L>();
+    auto kern = frame_cl_kernel<Q, L, OP, PROBE>;
     static bool attr = false;
     if (!attr) {
         PTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -241,7 +255,7 @@ void launch_cl_t(Plan& p, const FrameArgs<float>& a, int count, const float* amp
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)count * Q);
-    cfg.blockDim = dim3(64 * Q);
+    cfg.blockDim = dim3(Q * L);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = p.stream;
     cudaLaunchAttribute at[1];
@@ -251,15 +265,32 @@ void launch_cl_t(Plan& p, const FrameArgs<float>& a, int count, const float* amp
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    PTG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, amp_perm));
+    PTG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, amp_perm, tw));
+}
+
+template <int Q, int L, int OP>
+void launch_cl_ql(Plan& p, const FrameArgs<float>& a, int count, const float* ap, const float2* tw) {
+    if (a.probe) launch_cl_t<Q, L, OP, true>(p, a, count, ap, tw);
+    else launch_cl_t<Q, L, OP, false>(p, a, count, ap, tw);
 }
 
 template <int OP>
 void launch_cl(Plan& p, const FrameArgs<float>& a, int count, const float* data) {
     const float* ap = cl_amp(p, data);
-    const bool pr = a.probe != nullptr;
-    if (p.M == 128) pr ? launch_cl_t<2, OP, true>(p, a, count, ap) : launch_cl_t<2, OP, false>(p, a, count, ap);
-    else pr ? launch_cl_t<4, OP, true>(p, a, count, ap) : launch_cl_t<4, OP, false>(p, a, count, ap);
+    if (!p.cl_tw.p) {   // W_M^i, i < M, in fp64 rounded once
+        std::vector<float> h(2 * (size_t)p.M);
+        for (int i = 0; i < p.M; ++i) {
+            const double th = 2.0 * M_PI * i / p.M;
+            h[2 * i] = (float)std::cos(th);
+            h[2 * i + 1] = (float)-std::sin(th);
+        }
+        p.cl_tw.alloc(h.size() * sizeof(float));
+        PTG_CUDA(cudaMemcpy(p.cl_tw.p, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    const float2* tw = p.cl_tw.as<const float2>();
+    const int L = cl_line(p);
+    if (p.M == 128) L == 32 ? launch_cl_ql<4, 32, OP>(p, a, count, ap, tw) : launch_cl_ql<2, 64, OP>(p, a, count, ap, tw);
+    else L == 32 ? launch_cl_ql<8, 32, OP>(p, a, count, ap, tw) : launch_cl_ql<4, 64, OP>(p, a, count, ap, tw);
 }
 
 // objective frame kernel: TMA/register path for complex64 patch frames up to
@@ -756,7 +787,7 @@ void build_chunks(Plan& p) {
         p.chunks.clear();
         p.chunks.push_back(std::move(c));
         p.stash.alloc(p.celem());
-        p.misfit_per_pos = p.cl ? p.M / 64 : 1;
+        p.misfit_per_pos = p.cl ? p.M / 32 : 1;
         p.misfit.alloc(std::max<size_t>(1, (size_t)p.N * p.misfit_per_pos) * sizeof(double));
         p.dotp.alloc((size_t)kPlaneBlocks * sizeof(double));
         return;
@@ -817,7 +848,7 @@ void build_chunks(Plan& p) {
         p.chunks.push_back(std::move(c));
     }
     p.stash.alloc(std::max<size_t>(1, (size_t)cs * p.w * stash_pitch(p.w)) * p.celem());
-    p.misfit_per_pos = p.cl ? p.M / 64 : p.mp ? p.M / kMpLines : 1;
+    p.misfit_per_pos = p.cl ? p.M / 32 : p.mp ? p.M / kMpLines : 1;
     if (p.mp) {   // ~64 MiB of whole-frame scratch: stays L2-resident between passes
         const size_t fb = p.MM() * p.celem();
         p.mp_chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(p.N, 1), ((size_t)64 << 20) / fb));

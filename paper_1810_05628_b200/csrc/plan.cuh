@@ -116,8 +116,9 @@ struct Plan {
     // amplitudes permuted into its frequency order, rebuilt when the source
     // buffer or the data generation changes
     bool cl = false;
-    DevMem amp_cl;
+    DevMem amp_cl, cl_tw;
     const void* amp_cl_src = nullptr;
+    int amp_cl_line = 0;
     uint64_t amp_cl_gen = ~0ull;
     uint64_t data_gen = 0;   // bumped whenever amp / inten are rewritten
 
