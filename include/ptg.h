@@ -157,6 +157,8 @@ typedef struct {
     double grad_tol_rel, grad_tol_abs;
     int lbfgs_memory, linesearch_max;
     double max_weighted;
+    int cg_max_iters;      /* truncatedNewton inner CG (cgMaxIters) */
+    double cg_rel_tol;     /* cgRelTol */
 } ptg_solver_cfg;
 /* MgoptConfig (multigrid.hpp:39-49) */
 typedef struct {
@@ -188,6 +190,12 @@ void ptg_driver_cfg_default(ptg_driver_cfg *c);
 int ptg_lbfgs(ptg_plan *plan, int metric, const double *v, const double *z0,
               const ptg_solver_cfg *cfg, double *z_out, double *grad_out, ptg_report *rep,
               ptg_hist *hist, int hist_cap);
+
+/* truncatedNewton (solvers.hpp:101-104): Newton-CG with finite-difference
+ * Hessian-vector products (one counted gradient evaluation each), GPU-resident. */
+int ptg_truncated_newton(ptg_plan *plan, int metric, const double *v, const double *z0,
+                         const ptg_solver_cfg *cfg, double *z_out, double *grad_out, ptg_report *rep,
+                         ptg_hist *hist, int hist_cap);
 
 typedef struct ptg_hier ptg_hier;
 /* buildHierarchy (multigrid.hpp:61-62): coarse levels built ON DEVICE by

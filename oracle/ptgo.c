@@ -532,6 +532,8 @@ void ptgo_solver_cfg_default(ptgo_solver_cfg *c) {
     c->lbfgs_memory = 25;
     c->linesearch_max = 50;
     c->max_weighted = INFINITY;
+    c->cg_max_iters = 20;
+    c->cg_rel_tol = 0.1;
 }
 
 /* solvers.cpp:61-85 */
@@ -684,6 +686,104 @@ int ptgo_lbfgs(const ptgo_counted *obj, const double *z0, const ptgo_solver_cfg 
 done:
     for (int i = 0; i < np; ++i) { free(pairs[i].s); free(pairs[i].y); }
     free(z); free(g); free(dir); free(nz); free(ng); free(alpha); free(pairs);
+    return rc;
+}
+
+/* solvers.cpp:143-227: Newton-CG, each Hessian-vector product a counted
+ * gradient evaluation at z + delta v (delta = 1e-6 (1 + |z|) / |v|) */
+int ptgo_truncated_newton(const ptgo_counted *obj, const double *z0, const ptgo_solver_cfg *cfg,
+                          ptgo_counter *ctr, const double *warm_value, const double *warm_grad,
+                          double *z_out, double *value_out, double *grad_out, ptgo_report *rep) {
+    const size_t len = obj->len;
+    const size_t bytes = sizeof(double) * 2 * len;
+    int rc = PTGO_OK;
+    double *z = (double *)malloc(bytes), *g = (double *)malloc(bytes), *x = (double *)malloc(bytes);
+    double *r = (double *)malloc(bytes), *p = (double *)malloc(bytes), *hp = (double *)malloc(bytes);
+    double *zp = (double *)malloc(bytes), *gp = (double *)malloc(bytes), *nz = (double *)malloc(bytes);
+    double *ng = (double *)malloc(bytes);
+    double cur;
+    if (!z || !g || !x || !r || !p || !hp || !zp || !gp || !nz || !ng) {
+        rc = fail(PTGO_NOMEM, "truncatedNewton: out of memory");
+        goto done;
+    }
+    memcpy(z, z0, bytes);
+    if (warm_value) {
+        cur = *warm_value;
+        memcpy(g, warm_grad, bytes);
+    } else if ((rc = counted_eval(obj, ctr, z, &cur, g)) != PTGO_OK) {
+        goto done;
+    }
+    if (!all_finite(g, len)) { rc = fail(PTGO_NUMERIC, "non-finite iterate in truncatedNewton"); goto done; }
+    const double grad_floor = cfg->grad_tol_abs * (1.0 + norm2(z0, len));
+    const double g0 = norm2(g, len);
+    double gnorm = g0;
+    if ((rc = push_hist(rep, ctr->weighted, cur, gnorm))) goto done;
+    int reason = PTGO_STOP_MAXITERS;
+#define SATISFIED(gn) ((gn) <= fmax(cfg->grad_tol_rel * g0, grad_floor))
+    if (SATISFIED(gnorm)) {
+        reason = PTGO_STOP_TOLERANCE;
+    } else {
+        for (int iter = 1; iter <= cfg->max_iters; ++iter) {
+            /* CG on H x = -g from x = 0 */
+            memset(x, 0, bytes);
+            scale_into(r, g, -1.0, len);
+            const double rhs_norm = norm2(r, len);
+            memcpy(p, r, bytes);
+            double rs = ptgo_dot_real(r, r, len);
+            for (int cg = 0; cg < cfg->cg_max_iters; ++cg) {
+                /* hessVec(p) */
+                const double vnorm = norm2(p, len);
+                if (vnorm == 0.0) {
+                    memset(hp, 0, bytes);
+                } else {
+                    const double delta = 1e-6 * (1.0 + norm2(z, len)) / vnorm;
+                    memcpy(zp, z, bytes);
+                    axpy(zp, delta, p, len);
+                    double vp;
+                    if ((rc = counted_eval(obj, ctr, zp, &vp, gp)) != PTGO_OK) goto done;
+                    sub_into(hp, gp, g, len);
+                    scale_into(hp, hp, 1.0 / delta, len);
+                }
+                const double php = ptgo_dot_real(p, hp, len);
+                if (php <= 0.0) {
+                    /* negative curvature: keep what CG built, or steepest descent at cg == 0 */
+                    if (cg == 0) memcpy(x, r, bytes);
+                    break;
+                }
+                const double step = rs / php;
+                axpy(x, step, p, len);
+                axpy(r, -step, hp, len);
+                const double rs_new = ptgo_dot_real(r, r, len);
+                if (sqrt(rs_new) <= cfg->cg_rel_tol * rhs_norm) break;
+                /* p = r + beta p, formed as a copy of r then axpy */
+                memcpy(zp, r, bytes);
+                axpy(zp, rs_new / rs, p, len);
+                memcpy(p, zp, bytes);
+                rs = rs_new;
+            }
+            if (norm2(x, len) == 0.0 || ptgo_dot_real(x, g, len) >= 0.0) scale_into(x, g, -1.0, len);
+            double a, val;
+            int stalled, trials;
+            rc = ptgo_linesearch(obj, z, x, ctr, cfg->linesearch_max, &cur, &a, &stalled, &trials, nz, &val, ng);
+            if (rc) goto done;
+            if (stalled) { reason = PTGO_STOP_STALL; break; }
+            if (!all_finite(nz, len)) { rc = fail(PTGO_NUMERIC, "non-finite iterate in truncatedNewton"); goto done; }
+            memcpy(z, nz, bytes);
+            memcpy(g, ng, bytes);
+            cur = val;
+            gnorm = norm2(g, len);
+            if ((rc = push_hist(rep, ctr->weighted, cur, gnorm))) goto done;
+            if (SATISFIED(gnorm)) { reason = PTGO_STOP_TOLERANCE; break; }
+            if (ctr->weighted >= cfg->max_weighted) { reason = PTGO_STOP_BUDGET; break; }
+        }
+    }
+#undef SATISFIED
+    if (rep) rep->reason = reason;
+    memcpy(z_out, z, bytes);
+    if (value_out) *value_out = cur;
+    if (grad_out) memcpy(grad_out, g, bytes);
+done:
+    free(z); free(g); free(x); free(r); free(p); free(hp); free(zp); free(gp); free(nz); free(ng);
     return rc;
 }
 

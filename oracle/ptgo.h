@@ -104,6 +104,8 @@ typedef struct {
     double grad_tol_rel, grad_tol_abs;
     int lbfgs_memory, linesearch_max;
     double max_weighted;   /* +inf for no budget */
+    int cg_max_iters;      /* truncatedNewton inner CG */
+    double cg_rel_tol;
 } ptgo_solver_cfg;
 
 void ptgo_solver_cfg_default(ptgo_solver_cfg *c);   /* solvers.hpp:56-66 */
@@ -119,6 +121,12 @@ int ptgo_linesearch(const ptgo_counted *obj, const double *z, const double *dir,
 int ptgo_lbfgs(const ptgo_counted *obj, const double *z0, const ptgo_solver_cfg *cfg,
                ptgo_counter *ctr, const double *warm_value, const double *warm_grad,
                double *z_out, double *value_out, double *grad_out, ptgo_report *rep);
+
+/* solvers.cpp:143-227 (Newton-CG with finite-difference Hessian-vector
+ * products, one counted evaluation each); warm (value, grad) optional */
+int ptgo_truncated_newton(const ptgo_counted *obj, const double *z0, const ptgo_solver_cfg *cfg,
+                          ptgo_counter *ctr, const double *warm_value, const double *warm_grad,
+                          double *z_out, double *value_out, double *grad_out, ptgo_report *rep);
 
 /* solvers.cpp:229-265 with Alg. 1's complex-probe weight */
 int ptgo_pie(const ptgo_problem *p, const double *z0, double gamma, int sweeps,

@@ -76,7 +76,8 @@ class _Report(C.Structure):
 
 class _SolverCfg(C.Structure):
     _fields_ = [("max_iters", C.c_int), ("grad_tol_rel", C.c_double), ("grad_tol_abs", C.c_double),
-                ("lbfgs_memory", C.c_int), ("linesearch_max", C.c_int), ("max_weighted", C.c_double)]
+                ("lbfgs_memory", C.c_int), ("linesearch_max", C.c_int), ("max_weighted", C.c_double),
+                ("cg_max_iters", C.c_int), ("cg_rel_tol", C.c_double)]
 
 
 class _MgCfg(C.Structure):
@@ -299,8 +300,7 @@ def solver_cfg(**kw) -> _SolverCfg:
 _FN = C.CFUNCTYPE(C.c_int, C.c_void_p, _dp, _dp, _dp)
 
 
-def lbfgs(p: Problem, z0, v=None, **cfg) -> SolveResult:
-    """solvers.cpp:87-141 on the (v-shifted) objective of ``p``."""
+def _solver(fname: str, p: Problem, z0, v, cfg) -> SolveResult:
     z0 = _c128(z0)
     v = _c128(v) if v is not None else None
     n = p.n
@@ -323,13 +323,23 @@ def lbfgs(p: Problem, z0, v=None, **cfg) -> SolveResult:
     z = np.zeros_like(z0)
     g = np.zeros_like(z0)
     val = C.c_double()
-    lib().ptgo_lbfgs.argtypes = [C.c_void_p, _dp, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                 _dp, C.c_void_p, _dp, C.c_void_p]
-    _check(lib().ptgo_lbfgs(C.byref(obj), _ptr(z0.view(np.float64)), C.byref(c), C.byref(ctr), None, None,
-                            _ptr(z.view(np.float64)), C.byref(val), _ptr(g.view(np.float64)),
-                            C.byref(rep)))
+    f = getattr(lib(), fname)
+    f.argtypes = [C.c_void_p, _dp, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, _dp, C.c_void_p, _dp,
+                  C.c_void_p]
+    _check(f(C.byref(obj), _ptr(z0.view(np.float64)), C.byref(c), C.byref(ctr), None, None,
+             _ptr(z.view(np.float64)), C.byref(val), _ptr(g.view(np.float64)), C.byref(rep)))
     hist, reason = _report(rep)
     return SolveResult(z, val.value, g, hist, reason, ctr.weighted, [ctr.per_level[0]])
+
+
+def lbfgs(p: Problem, z0, v=None, **cfg) -> SolveResult:
+    """solvers.cpp:87-141 on the (v-shifted) objective of ``p``."""
+    return _solver("ptgo_lbfgs", p, z0, v, cfg)
+
+
+def truncated_newton(p: Problem, z0, v=None, **cfg) -> SolveResult:
+    """solvers.cpp:143-227 on the (v-shifted) objective of ``p``."""
+    return _solver("ptgo_truncated_newton", p, z0, v, cfg)
 
 
 class Hierarchy:
@@ -517,6 +527,28 @@ def ref_lbfgs(metric, n, w, pos, data, z0, v=None, max_iters=100, grad_tol_rel=0
                                  C.c_double(max_weighted), _ptr(z.view(np.float64)), C.byref(val),
                                  _ptr(g.view(np.float64)), _ptr(hist), cap, C.byref(nh), C.byref(wt),
                                  C.byref(reason)))
+    return SolveResult(z, val.value, g, hist[: nh.value].copy(), reason.value, wt.value, [])
+
+
+def ref_truncated_newton(metric, n, w, pos, data, z0, v=None, max_iters=100, grad_tol_rel=0.0,
+                         grad_tol_abs=1e-13, linesearch_max=50, cg_max_iters=20, cg_rel_tol=0.1,
+                         max_weighted=float("inf")) -> SolveResult:
+    win = _win(pos, w)
+    data = _f64(data)
+    z0 = _c128(z0)
+    v = _c128(v) if v is not None else None
+    z = np.zeros_like(z0)
+    g = np.zeros_like(z0)
+    cap = max_iters + 2
+    hist = np.zeros((cap, 3))
+    nh = C.c_int()
+    val, wt = C.c_double(), C.c_double()
+    reason = C.c_int()
+    _check_ref(ref().ptref_truncated_newton(
+        metric, n, win.shape[0], _ptr(win, _ip), _ptr(data), _ptr(v.view(np.float64)) if v is not None else None,
+        _ptr(z0.view(np.float64)), max_iters, C.c_double(grad_tol_rel), C.c_double(grad_tol_abs), linesearch_max,
+        cg_max_iters, C.c_double(cg_rel_tol), C.c_double(max_weighted), _ptr(z.view(np.float64)), C.byref(val),
+        _ptr(g.view(np.float64)), _ptr(hist), cap, C.byref(nh), C.byref(wt), C.byref(reason)))
     return SolveResult(z, val.value, g, hist[: nh.value].copy(), reason.value, wt.value, [])
 
 

@@ -244,6 +244,38 @@ int ptref_lbfgs(int metric, int n, int N, const int32_t* win, const double* data
     });
 }
 
+// solvers.cpp:143-227 on the (optionally v-shifted) ptychographic objective
+int ptref_truncated_newton(int metric, int n, int N, const int32_t* win, const double* data,
+                           const double* v, const double* z0, int max_iters, double grad_tol_rel,
+                           double grad_tol_abs, int linesearch_max, int cg_max_iters, double cg_rel_tol,
+                           double max_weighted, double* z_out, double* value, double* grad, double* hist,
+                           int hist_cap, int* nhist, double* weighted, int* reason) {
+    return guard([&] {
+        ScanGeometry geo = geometryFrom(n, N, win, 1);
+        DiffractionStack st = stackFrom(n, N, data);
+        ComplexField vf;
+        if (v) vf = fieldFrom(v, n);
+        Objective obj{metric == 0 ? MetricKind::Distance : MetricKind::IntensityGaussian, &geo, &st,
+                      v ? &vf : nullptr};
+        SolverConfig cfg;
+        cfg.maxIters = max_iters;
+        cfg.gradTolRel = grad_tol_rel;
+        cfg.gradTolAbs = grad_tol_abs;
+        cfg.linesearchMax = linesearch_max;
+        cfg.cgMaxIters = cg_max_iters;
+        cfg.cgRelTol = cg_rel_tol;
+        cfg.maxWeightedEvals = max_weighted;
+        EvalCounter ctr;
+        SolverReport rep = truncatedNewton(counted(obj), fieldFrom(z0, n), cfg, ctr);
+        fieldTo(rep.finalIterate, z_out);
+        *value = rep.finalEval.value;
+        fieldTo(rep.finalEval.gradient, grad);
+        historyTo(rep, hist, hist_cap, nhist);
+        *weighted = ctr.weightedEvals;
+        *reason = reasonCode(rep.reason);
+    });
+}
+
 // multigrid.cpp:95-227 on a raster geometry (n, w, s)
 int ptref_mgopt(int metric, int n, int w, int s, const double* data, int depth, int k1, int k2,
                 int coarsest_max_iters, double budget, double grad_tol_rel, double grad_tol_abs,

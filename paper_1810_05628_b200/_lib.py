@@ -69,7 +69,8 @@ class Hist(C.Structure):
 
 class SolverCfg(C.Structure):
     _fields_ = [("max_iters", C.c_int), ("grad_tol_rel", C.c_double), ("grad_tol_abs", C.c_double),
-                ("lbfgs_memory", C.c_int), ("linesearch_max", C.c_int), ("max_weighted", C.c_double)]
+                ("lbfgs_memory", C.c_int), ("linesearch_max", C.c_int), ("max_weighted", C.c_double),
+                ("cg_max_iters", C.c_int), ("cg_rel_tol", C.c_double)]
 
 
 class MgCfg(C.Structure):
@@ -99,7 +100,7 @@ EXPORTS = [
     "ptg_restrict_field", "ptg_prolong_field", "ptg_restrict_data",
     "ptg_restrict_field_device", "ptg_prolong_field_device", "ptg_restrict_data_device",
     "ptg_solver_cfg_default", "ptg_mg_cfg_default", "ptg_driver_cfg_default",
-    "ptg_lbfgs", "ptg_hier_create", "ptg_hier_destroy", "ptg_hier_level",
+    "ptg_lbfgs", "ptg_truncated_newton", "ptg_hier_create", "ptg_hier_destroy", "ptg_hier_level",
     "ptg_mgopt_driver", "ptg_mgopt_cycle_device",
 ]
 
@@ -144,6 +145,8 @@ def lib() -> C.CDLL:
     L.ptg_driver_cfg_default.restype = None
     L.ptg_lbfgs.argtypes = [_vp, C.c_int, _vp, _vp, C.POINTER(SolverCfg), _vp, _vp, C.POINTER(Report),
                             C.POINTER(Hist), C.c_int]
+    L.ptg_truncated_newton.argtypes = [_vp, C.c_int, _vp, _vp, C.POINTER(SolverCfg), _vp, _vp,
+                                       C.POINTER(Report), C.POINTER(Hist), C.c_int]
     L.ptg_hier_create.argtypes = [_vp, C.c_int, C.c_int, C.POINTER(MgCfg), C.POINTER(_vp)]
     L.ptg_hier_destroy.argtypes = [_vp]
     L.ptg_hier_level.argtypes = [_vp, C.c_int, C.POINTER(_vp)]

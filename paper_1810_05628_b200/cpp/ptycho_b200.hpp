@@ -272,6 +272,8 @@ struct SolverConfig {
     int maxIters = 100;
     double gradTolRel = 0.0, gradTolAbs = 1e-13;
     int lbfgsMemory = 25, linesearchMax = 50;
+    int cgMaxIters = 20;
+    double cgRelTol = 0.1;
     double maxWeightedEvals = std::numeric_limits<double>::infinity();
 };
 
@@ -311,19 +313,32 @@ inline SolverReport pie(const ComplexField& z0, const ScanGeometry& g, const Dif
     return detail::report(r, h, std::move(z), ctr);
 }
 
-// solvers.cpp:87-141 on the (optionally shifted) ptychographic objective, GPU-resident
-inline SolverReport lbfgs(const Objective& o, const ComplexField& z0, const SolverConfig& cfg, EvalCounter& ctr) {
-    auto plan = detail::make_plan(o, z0.n());
-    ptg_solver_cfg c{cfg.maxIters, cfg.gradTolRel, cfg.gradTolAbs, cfg.lbfgsMemory, cfg.linesearchMax,
-                     cfg.maxWeightedEvals};
+namespace detail {
+template <class F>
+inline SolverReport solve(F fn, const Objective& o, const ComplexField& z0, const SolverConfig& cfg,
+                          EvalCounter& ctr) {
+    auto plan = make_plan(o, z0.n());
+    ptg_solver_cfg c{cfg.maxIters,        cfg.gradTolRel,  cfg.gradTolAbs, cfg.lbfgsMemory,
+                     cfg.linesearchMax,   cfg.maxWeightedEvals, cfg.cgMaxIters, cfg.cgRelTol};
     ComplexField z(z0.n()), g(z0.n());
     std::vector<ptg_hist> h(cfg.maxIters + 2);
     ptg_report r{};
-    check(ptg_lbfgs(plan.get(), detail::metric_of(o.kind),
-                    o.shift ? reinterpret_cast<const double*>(o.shift->data()) : nullptr,
-                    reinterpret_cast<const double*>(z0.data()), &c, reinterpret_cast<double*>(z.data()),
-                    reinterpret_cast<double*>(g.data()), &r, h.data(), (int)h.size()));
-    return detail::report(r, h, std::move(z), ctr);
+    check(fn(plan.get(), metric_of(o.kind), o.shift ? reinterpret_cast<const double*>(o.shift->data()) : nullptr,
+             reinterpret_cast<const double*>(z0.data()), &c, reinterpret_cast<double*>(z.data()),
+             reinterpret_cast<double*>(g.data()), &r, h.data(), (int)h.size()));
+    return report(r, h, std::move(z), ctr);
+}
+}  // namespace detail
+
+// solvers.cpp:87-141 on the (optionally shifted) ptychographic objective, GPU-resident
+inline SolverReport lbfgs(const Objective& o, const ComplexField& z0, const SolverConfig& cfg, EvalCounter& ctr) {
+    return detail::solve(ptg_lbfgs, o, z0, cfg, ctr);
+}
+
+// solvers.cpp:143-227 (Newton-CG, finite-difference Hessian-vector products), GPU-resident
+inline SolverReport truncatedNewton(const Objective& o, const ComplexField& z0, const SolverConfig& cfg,
+                                    EvalCounter& ctr) {
+    return detail::solve(ptg_truncated_newton, o, z0, cfg, ctr);
 }
 
 // ------------------------------------------------------------ multigrid.hpp

@@ -105,6 +105,8 @@ void ptg_solver_cfg_default(ptg_solver_cfg* c) {
     c->lbfgs_memory = 25;
     c->linesearch_max = 50;
     c->max_weighted = std::numeric_limits<double>::infinity();
+    c->cg_max_iters = 20;
+    c->cg_rel_tol = 0.1;
 }
 
 void ptg_mg_cfg_default(ptg_mg_cfg* c) {
@@ -399,6 +401,35 @@ int ptg_lbfgs(ptg_plan* plan, int metric, const double* v, const double* z0,
         ptg::Counter ctr;
         std::vector<ptg_hist> h;
         ptg::SolveOut o = ptg::d_lbfgs(obj, zd.p, c, ctr, nullptr, nullptr, zo.p, go.p, &h);
+        if (z_out) ptg::plan_download_c128(p, zo.p, z_out);
+        if (grad_out) ptg::plan_download_c128(p, go.p, grad_out);
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+        fill_report(rep, ctr, o.value, o.reason, copy_hist(h, hist, hist_cap));
+    });
+}
+
+int ptg_truncated_newton(ptg_plan* plan, int metric, const double* v, const double* z0,
+                         const ptg_solver_cfg* cfg, double* z_out, double* grad_out, ptg_report* rep,
+                         ptg_hist* hist, int hist_cap) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        ptg_solver_cfg c;
+        if (cfg) c = *cfg;
+        else ptg_solver_cfg_default(&c);
+        const size_t len = p.nn();
+        ptg::DVec zd(p, len), vd, zo(p, len), go(p, len);
+        ptg::plan_upload_c128(p, z0, zd.p);
+        if (v) {
+            vd.alloc(p, len);
+            ptg::plan_upload_c128(p, v, vd.p);
+        }
+        ptg::DObj obj;
+        obj.plan = &p;
+        obj.metric = metric;
+        obj.v = v ? vd.p : nullptr;
+        ptg::Counter ctr;
+        std::vector<ptg_hist> h;
+        ptg::SolveOut o = ptg::d_truncated_newton(obj, zd.p, c, ctr, nullptr, nullptr, zo.p, go.p, &h);
         if (z_out) ptg::plan_download_c128(p, zo.p, z_out);
         if (grad_out) ptg::plan_download_c128(p, go.p, grad_out);
         PTG_CUDA(cudaStreamSynchronize(p.stream));

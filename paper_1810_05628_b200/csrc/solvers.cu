@@ -197,6 +197,100 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     return out;
 }
 
+// ------------------------------------------------------- truncated Newton
+// solvers.cpp:143-227: CG on H x = -g from x = 0, H v ~ (grad(z + d v) - g)/d
+// with d = 1e-6 (1 + |z|)/|v| (one counted evaluation per product), truncated
+// on negative curvature; steepest descent if CG gives nothing usable.
+SolveOut d_truncated_newton(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Counter& ctr,
+                            const double* warm_value, const void* warm_g, void* z_out, void* g_out,
+                            std::vector<ptg_hist>* hist) {
+    Plan& p = *obj.plan;
+    LaunchScope ls(p);
+    const size_t len = p.nn();
+    const int pr = p.prec;
+    cudaStream_t st = p.stream;
+    DVec z(p, len), g(p, len), x(p, len), r(p, len), pv(p, len), hp(p, len), zp(p, len), gp(p, len),
+        nz(p, len), ng(p, len);
+    dev_copy(pr, z.p, z0, len, st);
+    double cur;
+    if (warm_value) {
+        cur = *warm_value;
+        dev_copy(pr, g.p, warm_g, len, st);
+    } else {
+        cur = obj.eval(ctr, z.p, g.p);
+    }
+    if (plan_nonfinite(p, g.p, len)) raise(PTG_ERR_NUMERIC, "non-finite iterate in truncatedNewton");
+    const double grad_floor = cfg.grad_tol_abs * (1.0 + dnorm(p, z0));
+    const double g0 = dnorm(p, g.p);
+    double gnorm = g0;
+    if (hist) hist->push_back({ctr.weighted, cur, gnorm});
+    auto satisfied = [&](double gn) { return gn <= std::max(cfg.grad_tol_rel * g0, grad_floor); };
+    SolveOut out;
+    out.reason = PTG_STOP_MAXITERS;
+    if (satisfied(gnorm)) {
+        out.reason = PTG_STOP_TOLERANCE;
+    } else {
+        for (int iter = 1; iter <= cfg.max_iters; ++iter) {
+            dev_fill_zero(pr, x.p, len, st);
+            dev_scale(pr, r.p, g.p, -1.0, len, st);
+            const double rhs_norm = dnorm(p, r.p);
+            dev_copy(pr, pv.p, r.p, len, st);
+            double rs = plan_dot(p, r.p, r.p, len);
+            for (int cg = 0; cg < cfg.cg_max_iters; ++cg) {
+                const double vnorm = dnorm(p, pv.p);
+                if (vnorm == 0.0) {
+                    dev_fill_zero(pr, hp.p, len, st);
+                } else {
+                    const double delta = 1e-6 * (1.0 + dnorm(p, z.p)) / vnorm;
+                    dev_add_scaled(pr, zp.p, z.p, delta, pv.p, len, st);
+                    obj.eval(ctr, zp.p, gp.p);
+                    dev_sub(pr, hp.p, gp.p, g.p, len, st);
+                    dev_scale(pr, hp.p, hp.p, 1.0 / delta, len, st);
+                }
+                const double php = plan_dot(p, pv.p, hp.p, len);
+                if (php <= 0.0) {
+                    if (cg == 0) dev_copy(pr, x.p, r.p, len, st);
+                    break;
+                }
+                const double step = rs / php;
+                dev_axpy(pr, x.p, step, pv.p, len, st);
+                dev_axpy(pr, r.p, -step, hp.p, len, st);
+                const double rs_new = plan_dot(p, r.p, r.p, len);
+                if (std::sqrt(rs_new) <= cfg.cg_rel_tol * rhs_norm) break;
+                dev_copy(pr, zp.p, r.p, len, st);   // p = r + beta p
+                dev_axpy(pr, zp.p, rs_new / rs, pv.p, len, st);
+                std::swap(pv, zp);
+                rs = rs_new;
+            }
+            if (dnorm(p, x.p) == 0.0 || plan_dot(p, x.p, g.p, len) >= 0.0) dev_scale(pr, x.p, g.p, -1.0, len, st);
+            LsOut lsr = d_linesearch(obj, z.p, x.p, ctr, cfg.linesearch_max, &cur, nz.p, ng.p);
+            if (lsr.stalled) {
+                out.reason = PTG_STOP_STALL;
+                break;
+            }
+            if (plan_nonfinite(p, nz.p, len)) raise(PTG_ERR_NUMERIC, "non-finite iterate in truncatedNewton");
+            std::swap(z, nz);
+            std::swap(g, ng);
+            cur = lsr.value;
+            gnorm = dnorm(p, g.p);
+            if (hist) hist->push_back({ctr.weighted, cur, gnorm});
+            if (satisfied(gnorm)) {
+                out.reason = PTG_STOP_TOLERANCE;
+                break;
+            }
+            if (ctr.weighted >= cfg.max_weighted) {
+                out.reason = PTG_STOP_BUDGET;
+                break;
+            }
+        }
+    }
+    dev_copy(pr, z_out, z.p, len, st);
+    if (g_out) dev_copy(pr, g_out, g.p, len, st);
+    out.value = cur;
+    PTG_CUDA(cudaStreamSynchronize(st));
+    return out;
+}
+
 // ---------------------------------------------------------------- MG/OPT
 std::unique_ptr<Hier> hier_build(Plan& fine, int metric, int depth, const ptg_mg_cfg& opt) {
     if (depth < 1) raise(PTG_ERR_CONFIG, "hierarchy depth must be >= 1");

@@ -114,6 +114,11 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                  const double* warm_value, const void* warm_g, void* z_out, void* g_out,
                  std::vector<ptg_hist>* hist);
 
+// solvers.cpp:143-227 (Newton-CG, finite-difference Hessian-vector products)
+SolveOut d_truncated_newton(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Counter& ctr,
+                            const double* warm_value, const void* warm_g, void* z_out, void* g_out,
+                            std::vector<ptg_hist>* hist);
+
 struct Hier {
     Plan* fine = nullptr;
     std::vector<std::unique_ptr<Plan>> owned;   // levels 1..depth-1

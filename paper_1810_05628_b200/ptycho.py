@@ -207,7 +207,7 @@ class Plan:
     def pie_sweep_device(self, z, gamma: float = 0.0):
         check(lib().ptg_pie_sweep_device(self._h, _vp(z), float(gamma)))
 
-    def lbfgs(self, z0, v=None, metric: int = DISTANCE, **cfg) -> SolverReport:
+    def _solve(self, fn, z0, v, metric, cfg) -> SolverReport:
         c = L.SolverCfg()
         lib().ptg_solver_cfg_default(C.byref(c))
         for k, val in cfg.items():
@@ -219,12 +219,20 @@ class Plan:
         cap = c.max_iters + 2
         hist = (L.Hist * cap)()
         rep = L.Report()
-        check(lib().ptg_lbfgs(self._h, metric, _vp(v), z0.ctypes.data, C.byref(c), z.ctypes.data,
-                              g.ctypes.data, C.byref(rep), hist, cap))
+        check(fn(self._h, metric, _vp(v), z0.ctypes.data, C.byref(c), z.ctypes.data, g.ctypes.data,
+                 C.byref(rep), hist, cap))
         h = np.array([[hist[i].weighted, hist[i].value, hist[i].gnorm]
                       for i in range(min(rep.hist_len, cap))])
         return SolverReport(z, rep.final_value, h, STOP_NAMES[rep.reason], rep.weighted,
                             [int(rep.per_level[0])], g)
+
+    def lbfgs(self, z0, v=None, metric: int = DISTANCE, **cfg) -> SolverReport:
+        """lbfgs (solvers.hpp:92-95), GPU-resident."""
+        return self._solve(lib().ptg_lbfgs, z0, v, metric, cfg)
+
+    def truncated_newton(self, z0, v=None, metric: int = DISTANCE, **cfg) -> SolverReport:
+        """truncatedNewton (solvers.hpp:101-104), GPU-resident."""
+        return self._solve(lib().ptg_truncated_newton, z0, v, metric, cfg)
 
 
 class Hierarchy:

@@ -77,6 +77,11 @@ def main():
     r = ptgo.ref_lbfgs(0, n, w, pos, data, z0, v=out["eval_b_v"], max_iters=6)
     out["lbfgs_z"], out["lbfgs_hist"] = r.z, r.history
     out["lbfgs_meta"] = np.array([r.value, r.weighted, r.reason])
+    # truncatedNewton (solvers.cpp:143-227): Newton-CG with finite-difference
+    # Hessian-vector products, shifted objective, few outer / inner iterations
+    r = ptgo.ref_truncated_newton(0, n, w, pos, data, z0, v=out["eval_b_v"], max_iters=4, cg_max_iters=5)
+    out["tn_z"], out["tn_hist"] = r.z, r.history
+    out["tn_meta"] = np.array([r.value, r.weighted, r.reason])
     # MG/OPT from a non-degenerate start: at z = 1 a binary window's spectrum has
     # exact zeros where the theta(0) = 0 rule makes the gradient depend on FFT
     # rounding, so any other FFT cannot reproduce it

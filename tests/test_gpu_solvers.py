@@ -170,3 +170,35 @@ def test_fused_two_loop_matches_per_op(oracle, monkeypatch, precision):
     assert len(a.history) > 6
     assert np.array_equal(a.final_iterate, b.final_iterate)
     assert np.array_equal(a.history, b.history)
+
+
+def test_truncated_newton_ref_mode_vs_reference(gold):
+    """solvers.cpp:143-227 (Newton-CG, finite-difference Hessian-vector products)."""
+    plan, n, w, s = _ref_plan(gold)
+    r = plan.truncated_newton(gold["pie_z0"], v=gold["eval_b_v"], max_iters=4, cg_max_iters=5)
+    assert r.history.shape == gold["tn_hist"].shape
+    np.testing.assert_allclose(r.history[:, 0], gold["tn_hist"][:, 0], rtol=0)   # identical eval counts
+    np.testing.assert_allclose(r.history[:, 1:], gold["tn_hist"][:, 1:], rtol=1e-8)
+    assert r.weighted_evals == gold["tn_meta"][1]
+    assert rel_l2(r.final_iterate, gold["tn_z"]) <= 1e-8
+
+
+def test_truncated_newton_patch_c128_vs_oracle(oracle):
+    p, plan, cfg = _patch(oracle, "c128")
+    z0 = np.ones((cfg.n, cfg.n), np.complex128)
+    want = oracle.truncated_newton(p, z0, max_iters=3, cg_max_iters=6)
+    got = plan.truncated_newton(z0, max_iters=3, cg_max_iters=6)
+    assert got.weighted_evals == want.weighted
+    np.testing.assert_allclose(got.history, want.history, rtol=1e-8)
+    assert rel_l2(got.final_iterate, want.z) <= 1e-8
+
+
+def test_truncated_newton_c64_descends(oracle):
+    """complex64: the finite-difference Hessian products are fp32-noisy, so only
+    the solver contract is checked (monotone accepted values, accounting)."""
+    p, plan, cfg = _patch(oracle, "c64")
+    z0 = np.ones((cfg.n, cfg.n), np.complex128)
+    r = plan.truncated_newton(z0, max_iters=3, cg_max_iters=4)
+    vals = r.history[:, 1]
+    assert np.all(np.diff(vals) <= 0) and vals[-1] < vals[0]
+    assert r.weighted_evals == r.history[-1, 0]

@@ -77,6 +77,15 @@ def test_lbfgs_bitwise(oracle, gold):
     assert [r.value, r.weighted, r.reason] == list(gold["lbfgs_meta"])
 
 
+def test_truncated_newton_bitwise(oracle, gold):
+    n, w, s, pos, data = _geom(gold)
+    r = oracle.truncated_newton(oracle.Problem(n, n, w, pos, data), gold["pie_z0"], v=gold["eval_b_v"],
+                                max_iters=4, cg_max_iters=5)
+    assert np.array_equal(r.z, gold["tn_z"])
+    assert np.array_equal(r.history, gold["tn_hist"])
+    assert [r.value, r.weighted, r.reason] == list(gold["tn_meta"])
+
+
 @pytest.mark.parametrize("depth", [2, 3])
 def test_mgopt_bitwise(oracle, gold, depth):
     n, w, s, pos, data = _geom(gold)
