@@ -94,6 +94,11 @@ int ptg_plan_set_stream(ptg_plan *plan, void *stream);
 /* re-upload / replace the diffraction data (host or device pointer) */
 int ptg_plan_set_data(ptg_plan *plan, const void *host_data, int dtype);
 int ptg_plan_set_data_device(ptg_plan *plan, const void *dev_data, int dtype);
+/* loadRawStack (image_io.hpp:36, format :10-20) straight into the plan: the
+ * PTYF float64 stack is streamed through pinned double buffers (file read
+ * overlapping H2D copy + on-device conversion).  Errors: 2 (Io) for
+ * open/magic/truncation, 11 (Geometry) if the stack is not N patterns of side M. */
+int ptg_plan_load_ptyf(ptg_plan *plan, const char *path);
 /* bytes of HBM the plan holds, and its dims (any pointer may be NULL) */
 int ptg_plan_info(const ptg_plan *plan, int *n, int *M, int *w, int *N, int *precision,
                   size_t *device_bytes);

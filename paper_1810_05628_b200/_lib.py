@@ -93,7 +93,7 @@ class Report(C.Structure):
 EXPORTS = [
     "ptg_last_error", "ptg_version", "ptg_device_count",
     "ptg_plan_create", "ptg_plan_destroy", "ptg_plan_set_stream", "ptg_plan_set_data",
-    "ptg_plan_set_data_device", "ptg_plan_info", "ptg_plan_launch_count",
+    "ptg_plan_set_data_device", "ptg_plan_load_ptyf", "ptg_plan_info", "ptg_plan_launch_count",
     "ptg_plan_set_timing", "ptg_plan_get_timing",
     "ptg_eval", "ptg_eval_device", "ptg_project_modulus", "ptg_simulate", "ptg_simulate_device",
     "ptg_pie", "ptg_pie_sweep_device",
@@ -121,6 +121,7 @@ def lib() -> C.CDLL:
     L.ptg_plan_set_stream.argtypes = [_vp, _vp]
     L.ptg_plan_set_data.argtypes = [_vp, _vp, C.c_int]
     L.ptg_plan_set_data_device.argtypes = [_vp, _vp, C.c_int]
+    L.ptg_plan_load_ptyf.argtypes = [_vp, C.c_char_p]
     L.ptg_plan_info.argtypes = [_vp] + [C.POINTER(C.c_int)] * 5 + [C.POINTER(C.c_size_t)]
     L.ptg_plan_launch_count.argtypes = [_vp, C.POINTER(C.c_int64)]
     L.ptg_eval.argtypes = [_vp, C.c_int, _vp, _vp, _dp, _vp]

@@ -171,6 +171,10 @@ int ptg_plan_set_data_device(ptg_plan* plan, const void* dev_data, int dtype) {
     return guard([&] { ptg::plan_set_data_device(P(plan), dev_data, dtype); });
 }
 
+int ptg_plan_load_ptyf(ptg_plan* plan, const char* path) {
+    return guard([&] { ptg::plan_load_ptyf(P(plan), path); });
+}
+
 int ptg_plan_info(const ptg_plan* plan, int* n, int* M, int* w, int* N, int* precision,
                   size_t* device_bytes) {
     return guard([&] {

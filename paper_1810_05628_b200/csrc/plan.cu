@@ -967,6 +967,62 @@ void plan_set_data_device(Plan& p, const void* data, int dtype) {
     validate_and_amp(p);
 }
 
+// PTYF stack (image_io.hpp:10-20: "PTYF", u32 n, u32 channels, u32 0, then
+// channel-major row-major float64) streamed to the device through two pinned
+// staging buffers: the file read of chunk i+1 overlaps the H2D copy and the
+// on-device f64 -> plan-precision conversion of chunk i (image_io.cpp:184-196).
+void plan_load_ptyf(Plan& p, const char* path) {
+    LaunchScope ls(p);
+    const std::string where = std::string(path ? path : "(null)") + ": ";
+    FILE* f = path ? std::fopen(path, "rb") : nullptr;
+    if (!f) raise(PTG_ERR_IO, where + "cannot open for reading");
+    struct Closer {
+        FILE* f;
+        ~Closer() { std::fclose(f); }
+    } closer{f};
+    unsigned char hdr[16];
+    if (std::fread(hdr, 1, 4, f) != 4 || std::memcmp(hdr, "PTYF", 4) != 0) raise(PTG_ERR_IO, where + "not a PTYF file");
+    if (std::fread(hdr + 4, 1, 12, f) != 12) raise(PTG_ERR_IO, where + "truncated header");
+    auto u32 = [&](int o) { return (uint32_t)hdr[o] | (uint32_t)hdr[o + 1] << 8 | (uint32_t)hdr[o + 2] << 16 | (uint32_t)hdr[o + 3] << 24; };
+    const long long n = u32(4), ch = u32(8);
+    if (n < 1 || ch < 1) raise(PTG_ERR_IO, where + "bad PTYF dimensions");
+    if (n != p.M || ch != p.N)
+        raise(PTG_ERR_GEOMETRY, where + "stack of " + std::to_string(ch) + " patterns of side " + std::to_string(n) +
+                                    " does not match the plan (" + std::to_string(p.N) + " x " + std::to_string(p.M) + ")");
+    const size_t len = (size_t)p.N * p.MM();
+    p.inten.ensure(std::max<size_t>(1, len) * p.relem());
+    const size_t chunk = std::min<size_t>(len, (size_t)4 << 20);   // doubles per chunk (32 MiB)
+    HostPinned hb[2];
+    DevMem db[2];
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    for (int b = 0; b < 2; ++b) {
+        hb[b].ensure(chunk * sizeof(double));
+        db[b].alloc(chunk * sizeof(double));
+        PTG_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+    }
+    struct EvFree {
+        cudaEvent_t* e;
+        ~EvFree() { for (int b = 0; b < 2; ++b) if (e[b]) cudaEventDestroy(e[b]); }
+    } evfree{ev};
+    size_t done = 0;
+    for (int i = 0; done < len; ++i) {
+        const int b = i & 1;
+        const size_t cnt = std::min(chunk, len - done);
+        if (i >= 2) PTG_CUDA(cudaEventSynchronize(ev[b]));   // buffer b's previous copy has drained
+        if (std::fread(hb[b].p, sizeof(double), cnt, f) != cnt) {
+            PTG_CUDA(cudaStreamSynchronize(p.stream));
+            p.amp_valid = p.inten_valid = false;
+            raise(PTG_ERR_IO, where + "truncated payload");
+        }
+        PTG_CUDA(cudaMemcpyAsync(db[b].p, hb[b].p, cnt * sizeof(double), cudaMemcpyHostToDevice, p.stream));
+        dev_real_convert(p.prec, static_cast<unsigned char*>(p.inten.p) + done * p.relem(), PTG_F64, db[b].p, cnt,
+                         p.stream);
+        PTG_CUDA(cudaEventRecord(ev[b], p.stream));
+        done += cnt;
+    }
+    validate_and_amp(p);   // synchronises the stream
+}
+
 void plan_set_data_host(Plan& p, const void* data, int dtype) {
     const size_t len = (size_t)p.N * p.MM();
     if (!len) {

@@ -154,6 +154,7 @@ std::unique_ptr<Plan> plan_create(const ptg_plan_desc& d);
 std::unique_ptr<Plan> plan_coarsen(Plan& fine);
 void plan_set_data_host(Plan& p, const void* data, int dtype);
 void plan_set_data_device(Plan& p, const void* data, int dtype);
+void plan_load_ptyf(Plan& p, const char* path);   // PTYF stack file, streamed upload
 void plan_ensure(Plan& p, int metric);   // make amp / inten valid for metric
 
 // objective + gradient on device buffers (plan precision); grad may be null

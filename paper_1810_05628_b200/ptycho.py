@@ -19,6 +19,7 @@ everything resident.  Every call goes to the GPU; there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -118,6 +119,10 @@ class Plan:
             a = a.astype(np.float64)
         check(lib().ptg_plan_set_data(self._h, a.ctypes.data,
                                       L.PTG_F32 if a.dtype == np.float32 else L.PTG_F64))
+
+    def load_ptyf(self, path):
+        """loadRawStack (image_io.hpp:36) streamed straight into the plan's device data."""
+        check(lib().ptg_plan_load_ptyf(self._h, os.fsencode(path)))
 
     def set_data_device(self, data_tensor):
         import torch
@@ -330,3 +335,17 @@ def device_count() -> int:
     c = C.c_int()
     check(lib().ptg_device_count(C.byref(c)))
     return c.value
+
+
+def write_ptyf(path, stack) -> None:
+    """saveRawStack (image_io.hpp:37, format :10-20): "PTYF", u32 n, u32 k, u32 0,
+    then k row-major float64 n x n planes (little endian)."""
+    a = np.ascontiguousarray(stack, dtype="<f8")
+    if a.ndim == 2:
+        a = a[None]
+    k, n, n2 = a.shape
+    if n != n2 or k < 1:
+        raise ValueError("write_ptyf: expected a stack of square patterns")
+    with open(path, "wb") as f:
+        f.write(b"PTYF" + np.array([n, k, 0], "<u4").tobytes())
+        f.write(a.tobytes())

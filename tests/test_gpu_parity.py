@@ -212,3 +212,38 @@ def test_transfers_bitexact(oracle):
     assert np.array_equal(restrict_field(prolong_field(c)), c)   # multigrid.hpp:11-13
     d = np.abs(np.random.default_rng(9).normal(size=(5, 32, 32)))
     assert np.array_equal(restrict_data(d), oracle.restrict_data(d))
+
+
+def test_ptyf_streamed_upload(tmp_path, oracle):
+    """loadRawStack (image_io.cpp:184-196) streamed into the plan == in-memory upload;
+    the reference's error classes for bad files."""
+    from paper_1810_05628_b200 import GeometryError, IoError, Plan, synth, write_ptyf
+    cfg = synth.small_config(precision="c64")
+    obj, probe, pos = synth.make_inputs(cfg)
+    data = oracle.simulate(cfg.n, cfg.M, cfg.w, pos, obj, probe)
+    path = tmp_path / "stack.ptyf"
+    write_ptyf(path, data)
+    a = Plan(cfg.n, cfg.M, cfg.w, pos, data, probe, precision="c64")
+    b = Plan(cfg.n, cfg.M, cfg.w, pos, None, probe, precision="c64")
+    b.load_ptyf(path)
+    z = rand_field(cfg.n, seed=5)
+    va, ga = a.evaluate(z)
+    vb, gb = b.evaluate(z)
+    assert va == vb and np.array_equal(ga, gb)
+    bad = tmp_path / "bad.ptyf"
+    bad.write_bytes(b"NOPE" + bytes(12))
+    with pytest.raises(IoError):
+        b.load_ptyf(bad)
+    with pytest.raises(IoError):
+        b.load_ptyf(tmp_path / "missing.ptyf")
+    trunc = tmp_path / "trunc.ptyf"
+    trunc.write_bytes(path.read_bytes()[:-8])
+    with pytest.raises(IoError):
+        b.load_ptyf(trunc)
+    other = tmp_path / "other.ptyf"
+    write_ptyf(other, data[:-1])
+    with pytest.raises(GeometryError):
+        b.load_ptyf(other)
+    b.load_ptyf(path)   # the plan stays usable after failed loads
+    vc, gc = b.evaluate(z)
+    assert vc == va
