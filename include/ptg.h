@@ -155,6 +155,26 @@ int ptg_restrict_field_device(int precision, const void *fine, int n, void *coar
 int ptg_prolong_field_device(int precision, const void *coarse, int nH, void *fine, void *stream);
 int ptg_restrict_data_device(int dtype, const void *fine, int N, int M, void *coarse, void *stream);
 
+/* ------------------------------------------------------------- diagnostics */
+/* metrics.hpp:9-24 on the device: relativeError, magnitudeRelError and
+ * phaseSSIM (11x11 Gaussian window, sigma 1.5, L = pi/2), fp64 arithmetic.
+ * Errors: 12 (Domain) for empty fields / zero reference, 13 (Metric) for
+ * phaseSSIM with n < 11. */
+#define PTG_METRIC_RELATIVE_ERROR 1u
+#define PTG_METRIC_MAGNITUDE_REL_ERROR 2u
+#define PTG_METRIC_PHASE_SSIM 4u
+#define PTG_METRIC_ALL 7u
+typedef struct {
+    double relative_error, magnitude_rel_error, phase_ssim;
+} ptg_metrics;
+/* device fields in `precision` (n x n complex), stream may be NULL */
+int ptg_metrics_device(int precision, const void *z, const void *z_true, int n, unsigned mask,
+                       ptg_metrics *out, void *stream);
+/* host complex128 fields */
+int ptg_metrics_host(const double *z, const double *z_true, int n, unsigned mask, ptg_metrics *out);
+/* canonicalPhase (metrics.hpp:15-18): host complex128 in, host fp64 n x n out */
+int ptg_canonical_phase(const double *z, int n, double *out);
+
 /* -------------------------------------------------------- solvers, MG/OPT */
 /* SolverConfig (solvers.hpp:56-66) */
 typedef struct {

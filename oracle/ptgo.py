@@ -570,3 +570,19 @@ def ref_mgopt(metric, n, w, s, data, z0, depth, k1=1, k2=1, coarsest_max_iters=0
                                  C.byref(reason)))
     return SolveResult(z, val.value, None, hist[: min(nh.value, cap)].copy(), reason.value, wt.value,
                        [int(per[l]) for l in range(depth)])
+
+
+def ref_metrics(z, z_true):
+    """metrics.cpp:67-136 via the reference: (relativeError, magnitudeRelError, phaseSSIM)."""
+    z = _c128(z)
+    zt = _c128(z_true)
+    out = np.zeros(3)
+    _check_ref(ref().ptref_metrics(z.shape[0], _ptr(z.view(np.float64)), _ptr(zt.view(np.float64)), _ptr(out)))
+    return tuple(out)
+
+
+def ref_canonical_phase(z):
+    z = _c128(z)
+    out = np.zeros(z.shape)
+    _check_ref(ref().ptref_canonical_phase(z.shape[0], _ptr(z.view(np.float64)), _ptr(out)))
+    return out

@@ -19,6 +19,7 @@
 #include "ptycho/field.hpp"
 #include "ptycho/forward.hpp"
 #include "ptycho/kernels.hpp"
+#include "ptycho/metrics.hpp"
 #include "ptycho/multigrid.hpp"
 #include "ptycho/objectives.hpp"
 #include "ptycho/solvers.hpp"
@@ -307,6 +308,23 @@ int ptref_mgopt(int metric, int n, int w, int s, const double* data, int depth, 
             per_level[l] = it == ctr.perLevelEvals.end() ? 0 : it->second;
         }
         *reason = reasonCode(rep.reason);
+    });
+}
+
+// metrics.cpp:67-136 (diagnostics): out = {relativeError, magnitudeRelError, phaseSSIM}
+int ptref_metrics(int n, const double* z, const double* z_true, double* out) {
+    return guard([&] {
+        const ComplexField a = fieldFrom(z, n), b = fieldFrom(z_true, n);
+        out[0] = relativeError(a, b);
+        out[1] = magnitudeRelError(a, b);
+        out[2] = phaseSSIM(a, b);
+    });
+}
+
+int ptref_canonical_phase(int n, const double* z, double* out) {
+    return guard([&] {
+        const RealGrid p = canonicalPhase(fieldFrom(z, n));
+        for (std::size_t i = 0; i < p.size(); ++i) out[i] = p[i];
     });
 }
 

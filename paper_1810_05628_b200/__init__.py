@@ -9,8 +9,10 @@ call that needs libptg loads it and fails loudly if it is missing.
 from .ptycho import (DISTANCE, INTENSITY, ConfigError, CudaError, DomainError, Error,  # noqa: F401
                      GeometryError, Hierarchy, IoError, MetricError, NumericError, Plan,
                      SolverReport, device_count, prolong_field, restrict_data, restrict_field,
-                     write_ptyf)
+                     write_ptyf, metrics, metrics_device, relative_error, magnitude_rel_error,
+                     phase_ssim, canonical_phase)
 
 __all__ = ["Plan", "Hierarchy", "SolverReport", "restrict_field", "prolong_field", "restrict_data",
            "DISTANCE", "INTENSITY", "Error", "ConfigError", "GeometryError", "DomainError",
-           "MetricError", "IoError", "NumericError", "CudaError", "device_count", "write_ptyf"]
+           "MetricError", "IoError", "NumericError", "CudaError", "device_count", "write_ptyf",
+           "metrics", "metrics_device", "relative_error", "magnitude_rel_error", "phase_ssim", "canonical_phase"]

@@ -67,6 +67,13 @@ class Hist(C.Structure):
     _fields_ = [("weighted", C.c_double), ("value", C.c_double), ("gnorm", C.c_double)]
 
 
+class Metrics(C.Structure):
+    _fields_ = [("relative_error", C.c_double), ("magnitude_rel_error", C.c_double), ("phase_ssim", C.c_double)]
+
+
+PTG_METRIC_RELATIVE_ERROR, PTG_METRIC_MAGNITUDE_REL_ERROR, PTG_METRIC_PHASE_SSIM, PTG_METRIC_ALL = 1, 2, 4, 7
+
+
 class SolverCfg(C.Structure):
     _fields_ = [("max_iters", C.c_int), ("grad_tol_rel", C.c_double), ("grad_tol_abs", C.c_double),
                 ("lbfgs_memory", C.c_int), ("linesearch_max", C.c_int), ("max_weighted", C.c_double),
@@ -100,6 +107,7 @@ EXPORTS = [
     "ptg_restrict_field", "ptg_prolong_field", "ptg_restrict_data",
     "ptg_restrict_field_device", "ptg_prolong_field_device", "ptg_restrict_data_device",
     "ptg_solver_cfg_default", "ptg_mg_cfg_default", "ptg_driver_cfg_default",
+    "ptg_metrics_device", "ptg_metrics_host", "ptg_canonical_phase",
     "ptg_lbfgs", "ptg_truncated_newton", "ptg_hier_create", "ptg_hier_destroy", "ptg_hier_level",
     "ptg_mgopt_driver", "ptg_mgopt_cycle_device",
 ]
@@ -122,6 +130,9 @@ def lib() -> C.CDLL:
     L.ptg_plan_set_data.argtypes = [_vp, _vp, C.c_int]
     L.ptg_plan_set_data_device.argtypes = [_vp, _vp, C.c_int]
     L.ptg_plan_load_ptyf.argtypes = [_vp, C.c_char_p]
+    L.ptg_metrics_device.argtypes = [C.c_int, _vp, _vp, C.c_int, C.c_uint, C.POINTER(Metrics), _vp]
+    L.ptg_metrics_host.argtypes = [_vp, _vp, C.c_int, C.c_uint, C.POINTER(Metrics)]
+    L.ptg_canonical_phase.argtypes = [_vp, C.c_int, _vp]
     L.ptg_plan_info.argtypes = [_vp] + [C.POINTER(C.c_int)] * 5 + [C.POINTER(C.c_size_t)]
     L.ptg_plan_launch_count.argtypes = [_vp, C.POINTER(C.c_int64)]
     L.ptg_eval.argtypes = [_vp, C.c_int, _vp, _vp, _dp, _vp]

@@ -11,6 +11,7 @@
 #include <string>
 
 #include "plan.cuh"
+#include "metrics.cuh"
 #include "solvers.cuh"
 #include "transfer.cuh"
 
@@ -409,6 +410,43 @@ int ptg_lbfgs(ptg_plan* plan, int metric, const double* v, const double* z0,
         if (grad_out) ptg::plan_download_c128(p, go.p, grad_out);
         PTG_CUDA(cudaStreamSynchronize(p.stream));
         fill_report(rep, ctr, o.value, o.reason, copy_hist(h, hist, hist_cap));
+    });
+}
+
+int ptg_metrics_device(int precision, const void* z, const void* z_true, int n, unsigned mask,
+                       ptg_metrics* out, void* stream) {
+    return guard([&] {
+        if (!out || !z || !z_true) ptg::raise(PTG_ERR_CONFIG, "ptg_metrics_device: null pointer");
+        ptg::dev_metrics(precision, z, z_true, n, mask, out, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int ptg_metrics_host(const double* z, const double* z_true, int n, unsigned mask, ptg_metrics* out) {
+    return guard([&] {
+        if (!out || !z || !z_true) ptg::raise(PTG_ERR_CONFIG, "ptg_metrics_host: null pointer");
+        if (n < 1) ptg::raise(PTG_ERR_DOMAIN, "metric: empty fields");
+        const size_t bytes = (size_t)n * n * 16;
+        void* d = nullptr;
+        PTG_CUDA(cudaMalloc(&d, 2 * bytes));
+        struct F { void* p; ~F() { cudaFree(p); } } f{d};
+        PTG_CUDA(cudaMemcpy(d, z, bytes, cudaMemcpyHostToDevice));
+        PTG_CUDA(cudaMemcpy(static_cast<char*>(d) + bytes, z_true, bytes, cudaMemcpyHostToDevice));
+        ptg::dev_metrics(PTG_C128, d, static_cast<char*>(d) + bytes, n, mask, out, nullptr);
+    });
+}
+
+int ptg_canonical_phase(const double* z, int n, double* out) {
+    return guard([&] {
+        if (!out || !z) ptg::raise(PTG_ERR_CONFIG, "ptg_canonical_phase: null pointer");
+        if (n < 1) ptg::raise(PTG_ERR_DOMAIN, "metric: empty fields");
+        const size_t len = (size_t)n * n;
+        void* d = nullptr;
+        PTG_CUDA(cudaMalloc(&d, len * 16 + len * 8));
+        struct F { void* p; ~F() { cudaFree(p); } } f{d};
+        PTG_CUDA(cudaMemcpy(d, z, len * 16, cudaMemcpyHostToDevice));
+        double* ph = reinterpret_cast<double*>(static_cast<char*>(d) + len * 16);
+        ptg::dev_canonical_phase(PTG_C128, d, n, ph, nullptr);
+        PTG_CUDA(cudaMemcpy(out, ph, len * 8, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -349,3 +349,56 @@ def write_ptyf(path, stack) -> None:
     with open(path, "wb") as f:
         f.write(b"PTYF" + np.array([n, k, 0], "<u4").tobytes())
         f.write(a.tobytes())
+
+
+# ------------------------------------------------------------ diagnostics
+def _square_pair(z, z_true):
+    z = _c128(z)
+    zt = _c128(z_true)
+    if z.ndim != 2 or z.shape[0] != z.shape[1]:
+        raise GeometryError("metric: fields must be square")
+    if z.shape != zt.shape:
+        raise DomainError("metric: field sizes differ")   # checkSameSize (metrics.cpp:17-20)
+    return z, zt
+
+
+def metrics(z, z_true, mask: int = L.PTG_METRIC_ALL) -> dict:
+    """metrics.hpp:9-24 computed on the GPU (host complex128 fields)."""
+    z, zt = _square_pair(z, z_true)
+    m = L.Metrics()
+    check(lib().ptg_metrics_host(z.ctypes.data, zt.ctypes.data, z.shape[0], mask, C.byref(m)))
+    return {"relative_error": m.relative_error, "magnitude_rel_error": m.magnitude_rel_error,
+            "phase_ssim": m.phase_ssim}
+
+
+def metrics_device(z, z_true, mask: int = L.PTG_METRIC_ALL, stream: int = 0) -> dict:
+    """The same on device tensors (complex64 or complex128, n x n) — no host copy of the fields."""
+    import torch
+    if z.shape != z_true.shape or z.dtype != z_true.dtype:
+        raise DomainError("metric: field sizes differ")
+    prec = {torch.complex64: L.PTG_C64, torch.complex128: L.PTG_C128}[z.dtype]
+    m = L.Metrics()
+    check(lib().ptg_metrics_device(prec, z.data_ptr(), z_true.data_ptr(), z.shape[0], mask, C.byref(m),
+                                   stream or None))
+    return {"relative_error": m.relative_error, "magnitude_rel_error": m.magnitude_rel_error,
+            "phase_ssim": m.phase_ssim}
+
+
+def relative_error(z, z_true) -> float:
+    return metrics(z, z_true, L.PTG_METRIC_RELATIVE_ERROR)["relative_error"]
+
+
+def magnitude_rel_error(z, z_true) -> float:
+    return metrics(z, z_true, L.PTG_METRIC_MAGNITUDE_REL_ERROR)["magnitude_rel_error"]
+
+
+def phase_ssim(z, z_true) -> float:
+    return metrics(z, z_true, L.PTG_METRIC_PHASE_SSIM)["phase_ssim"]
+
+
+def canonical_phase(z) -> np.ndarray:
+    """canonicalPhase (metrics.hpp:15-18) on the GPU."""
+    z = _c128(z)
+    out = np.empty(z.shape, np.float64)
+    check(lib().ptg_canonical_phase(z.ctypes.data, z.shape[0], out.ctypes.data))
+    return out

@@ -82,6 +82,16 @@ def main():
     r = ptgo.ref_truncated_newton(0, n, w, pos, data, z0, v=out["eval_b_v"], max_iters=4, cg_max_iters=5)
     out["tn_z"], out["tn_hist"] = r.z, r.history
     out["tn_meta"] = np.array([r.value, r.weighted, r.reason])
+    # diagnostics (metrics.cpp:67-136) on a reconstruction vs the truth and on a
+    # random 40x40 pair (phase maps with a full [-pi, pi] range)
+    out["met_a"] = np.array(ptgo.ref_metrics(out["tn_z"], out["eval_b_truth"]))
+    out["met_phase_a"] = ptgo.ref_canonical_phase(out["tn_z"])
+    rng = np.random.default_rng(77)
+    za = rng.normal(size=(40, 40)) + 1j * rng.normal(size=(40, 40))
+    zb = za + 0.3 * (rng.normal(size=(40, 40)) + 1j * rng.normal(size=(40, 40)))
+    out["met_za"], out["met_zb"] = za, zb
+    out["met_b"] = np.array(ptgo.ref_metrics(za, zb))
+    out["met_phase_b"] = ptgo.ref_canonical_phase(za)
     # MG/OPT from a non-degenerate start: at z = 1 a binary window's spectrum has
     # exact zeros where the theta(0) = 0 rule makes the gradient depend on FFT
     # rounding, so any other FFT cannot reproduce it
