@@ -23,6 +23,8 @@ LIB = os.path.join(LIBDIR, "libptg.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
            "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
+# PTG_NVCC_DEFS="-DFOO=1 ...": extra defines for kernel-variant experiments
+NVFLAGS += os.environ.get("PTG_NVCC_DEFS", "").split()
 
 
 def nvcc() -> str:

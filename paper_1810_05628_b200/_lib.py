@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libptg.so")
+# PTG_LIB: alternative build of the same library (A/B experiments on kernel variants)
+LIB_PATH = os.environ.get("PTG_LIB") or os.path.join(PKG, "lib", "libptg.so")
 
 PTG_OK = 0
 PTG_C64, PTG_C128 = 0, 1
