@@ -269,7 +269,9 @@ TEST_CASE("GPU evaluation is bitwise reproducible") {
 }
 
 int main() {
+    std::setvbuf(stdout, nullptr, _IONBF, 0);   // progress survives a crash
     for (auto& [name, fn] : cases()) {
+        std::printf("RUN %s\n", name.c_str());
         const int before = g_fail;
         try {
             fn();

@@ -149,9 +149,7 @@ int ptg_plan_destroy(ptg_plan* plan) {
         if (plan->p) {
             cudaSetDevice(plan->p->device);
             cudaStreamSynchronize(plan->p->stream);
-            cudaStream_t own = plan->p->own_stream;
-            plan->p.reset();
-            if (own) cudaStreamDestroy(own);
+            plan->p.reset();   // ~Plan releases the plan's own streams and events
         }
         delete plan;
     });
@@ -223,19 +221,7 @@ int ptg_plan_get_timing(ptg_plan* plan, double* frame_ms, int64_t* frame_launche
 int ptg_eval(ptg_plan* plan, int metric, const double* z, const double* v, double* value,
              double* grad) {
     return guard([&] {
-        ptg::Plan& p = P(plan);
-        const size_t bytes = p.nn() * p.celem();
-        p.zbuf.ensure(bytes);
-        p.gbuf.ensure(bytes);
-        ptg::plan_upload_c128(p, z, p.zbuf.p);
-        if (v) {
-            p.vbuf.ensure(bytes);
-            ptg::plan_upload_c128(p, v, p.vbuf.p);
-        }
-        ptg::plan_eval(p, metric, p.zbuf.p, v ? p.vbuf.p : nullptr, p.gbuf.p, p.value.as<double>());
-        if (grad) ptg::plan_download_c128(p, p.gbuf.p, grad);
-        const double val = ptg::plan_read_scalar(p, p.value.as<double>());
-        if (value) *value = val;
+        ptg::plan_eval_host(P(plan), metric, z, v, value, grad);
     });
 }
 

@@ -31,6 +31,10 @@ Plan::~Plan() {
         if (e.a) cudaEventDestroy(e.a);
         if (e.b) cudaEventDestroy(e.b);
     }
+    for (auto e : ev_band) cudaEventDestroy(e);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
+    if (own_stream) cudaStreamDestroy(own_stream);
 }
 
 void Plan::ev_begin(int kind) {
@@ -383,13 +387,18 @@ __global__ void __launch_bounds__(256) k_plane_reduce(const cplx<T>* __restrict_
                                                       const cplx<T>* __restrict__ v, const cplx<T>* __restrict__ z,
                                                       cplx<T>* __restrict__ grad, double* __restrict__ dotp,
                                                       const double* __restrict__ misfit, int N,
-                                                      double* value_out, unsigned int* counter) {
+                                                      double* value_out, unsigned int* counter,
+                                                      int block0) {
+    // logical block b = block0 + blockIdx.x of a fixed kPlaneBlocks partition:
+    // a launch may cover a subset of the blocks (banded host evaluation); the
+    // fused final value (value_out) needs the full grid in one launch
     __shared__ double red[8];
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int lin = threadIdx.x;
+    const int b = block0 + blockIdx.x;
     const size_t npairs = (nn + 1) / 2;
-    const size_t chunk = (npairs + gridDim.x - 1) / gridDim.x;
-    const size_t lo = blockIdx.x * chunk, hi = min(lo + chunk, npairs);
+    const size_t chunk = (npairs + kPlaneBlocks - 1) / kPlaneBlocks;
+    const size_t lo = min(npairs, b * chunk), hi = min(lo + chunk, npairs);
     double d = 0.0;
     for (size_t pr = lo + lin; pr < hi; pr += blockDim.x) {
         const size_t i = 2 * pr;
@@ -444,8 +453,9 @@ __global__ void __launch_bounds__(256) k_plane_reduce(const cplx<T>* __restrict_
     if (lin == 0) {
         double s = 0.0;
         for (int k = 0; k < 8; ++k) s += red[k];
-        dotp[blockIdx.x] = s;
+        dotp[b] = s;
     }
+    if (!value_out) return;   // partial launch: the value is formed by k_finalize
     __shared__ bool last;
     if (lin == 0) {
         __threadfence();
@@ -1103,7 +1113,7 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
             PTG_CUDA(cudaLaunchKernelEx(&cfg, k_plane_reduce<T>, p.planes.as<const C>(), p.ncolors, p.nn(),
                                         static_cast<const C*>(v), static_cast<const C*>(z), static_cast<C*>(grad),
                                         p.dotp.as<double>(), p.misfit.as<const double>(), p.N * p.misfit_per_pos,
-                                        value_dev, p.counter.as<unsigned int>()));
+                                        value_dev, p.counter.as<unsigned int>(), 0));
             p.ev_end();
             ++p.launches;
             return;
@@ -1162,6 +1172,148 @@ void plan_eval(Plan& p, int metric, const void* z, const void* v, void* grad, do
     if (!value_dev) value_dev = p.value.as<double>();
     if (p.prec == PTG_C64) eval_t<float>(p, metric, z, v, grad, value_dev);
     else eval_t<double>(p, metric, z, v, grad, value_dev);
+}
+
+// ------------------------------------------------------ banded host eval
+// ptg_eval with host complex128 buffers.  The object is uploaded in row bands
+// on a copy-in stream; as soon as the rows a group of frames reads are on the
+// device, that group runs (positions must be ordered by window row, as
+// raster / serpentine scans are); plane-reduce blocks run once every frame
+// reaching their pixel rows has run (a subset of the same fixed partition, so
+// the gradient and the value are bitwise those of plan_eval); finished
+// gradient rows go back on a copy-out stream while later bands compute.
+// Falls back to upload -> plan_eval -> download when a condition fails.
+template <typename T>
+static void eval_host_banded(Plan& p, int metric, const double* z, const double* v, double* value, double* grad) {
+    using C = cplx<T>;
+    const int n = p.n, w = p.w, N = p.N;
+    const size_t nn = p.nn(), npairs = (nn + 1) / 2, chunk = (npairs + kPlaneBlocks - 1) / kPlaneBlocks;
+    static const int K = getenv("PTG_BANDS") ? std::max(2, std::min(16, atoi(getenv("PTG_BANDS")))) : 4;   // object bands (more: host-bound)
+    const int H = (n + K - 1) / K;
+    if (!p.s_in) {
+        PTG_CUDA(cudaStreamCreateWithFlags(&p.s_in, cudaStreamNonBlocking));
+        PTG_CUDA(cudaStreamCreateWithFlags(&p.s_out, cudaStreamNonBlocking));
+    }
+    while (p.ev_band.size() < (size_t)(3 * K + 2)) {
+        cudaEvent_t e;
+        PTG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        p.ev_band.push_back(e);
+    }
+    cudaEvent_t* ev_in = p.ev_band.data();            // [K] band uploaded
+    cudaEvent_t* ev_out = p.ev_band.data() + K;       // [K] gradient rows converted
+    cudaEvent_t ev_start = p.ev_band[2 * K], ev_val = p.ev_band[2 * K + 1];
+    const size_t cb = p.celem();
+    p.zbuf.ensure(nn * cb);
+    p.gbuf.ensure(nn * cb);
+    if (v) p.vbuf.ensure(nn * cb);
+    p.stage.ensure(nn * 16 * (v ? 2 : 1));
+    p.stage_out.ensure(nn * 16);
+    double* st_z = p.stage.as<double>();
+    double* st_v = st_z + 2 * nn;
+    C* zd = p.zbuf.as<C>();
+    C* vd = v ? p.vbuf.as<C>() : nullptr;
+    C* gd = p.gbuf.as<C>();
+    const T* data = metric == PTG_DISTANCE ? p.amp.as<const T>() : p.inten.as<const T>();
+    // the copy streams start after work already queued on the plan's stream
+    PTG_CUDA(cudaEventRecord(ev_start, p.stream));
+    PTG_CUDA(cudaStreamWaitEvent(p.s_in, ev_start, 0));
+    PTG_CUDA(cudaStreamWaitEvent(p.s_out, ev_start, 0));
+    for (int b = 0; b < K; ++b) {
+        const size_t r0 = (size_t)std::min(n, b * H), r1 = (size_t)std::min(n, (b + 1) * H);
+        const size_t off = r0 * n, cnt = (r1 - r0) * n;
+        if (cnt) {
+            PTG_CUDA(cudaMemcpyAsync(st_z + 2 * off, z + 2 * off, cnt * 16, cudaMemcpyHostToDevice, p.s_in));
+            if (v) PTG_CUDA(cudaMemcpyAsync(st_v + 2 * off, v + 2 * off, cnt * 16, cudaMemcpyHostToDevice, p.s_in));
+        }
+        PTG_CUDA(cudaEventRecord(ev_in[b], p.s_in));
+    }
+    int f_done = 0, k_done = 0;
+    size_t rows_out = 0;   // gradient rows already converted for copy-out
+    FrameArgs<T> a = frame_args<T>(p, zd, data);
+    for (int b = 0; b < K; ++b) {
+        const int r1 = std::min(n, (b + 1) * H);
+        const size_t off = (size_t)std::min(n, b * H) * n, cnt = (size_t)r1 * n - off;
+        PTG_CUDA(cudaStreamWaitEvent(p.stream, ev_in[b], 0));
+        if (cnt) {
+            dev_from_c128(p.prec, zd + off, st_z + 2 * off, cnt, p.stream);
+            if (v) dev_from_c128(p.prec, vd + off, st_v + 2 * off, cnt, p.stream);
+        }
+        // frames whose windows lie in rows < r1 (all of them after the last band)
+        int f_end = f_done;
+        while (f_end < N && (b == K - 1 || p.pos_h[2 * f_end] + w <= r1)) ++f_end;
+        if (f_end > f_done) {
+            a.first = f_done;
+            if (metric == PTG_DISTANCE) launch_objective<T, OP_DISTANCE>(p, a, f_end - f_done, zd, data);
+            else launch_objective<T, OP_INTENSITY>(p, a, f_end - f_done, zd, data);
+            ++p.launches;
+            f_done = f_end;
+        }
+        // reduce blocks whose pixel rows no later frame reaches
+        const int next_row = f_done < N ? p.pos_h[2 * f_done] : n;   // first row a pending frame touches
+        int k_end = k_done;
+        while (k_end < kPlaneBlocks) {
+            const size_t hi = std::min(npairs, (size_t)(k_end + 1) * chunk);
+            const size_t last_pix = hi ? std::min(nn - 1, 2 * hi - 1) : 0;
+            if (f_done < N && (int)(last_pix / n) >= next_row) break;
+            ++k_end;
+        }
+        if (k_end > k_done) {
+            k_plane_reduce<T><<<k_end - k_done, 256, 0, p.stream>>>(
+                p.planes.as<const C>(), p.ncolors, nn, vd, zd, gd, p.dotp.as<double>(),
+                p.misfit.as<const double>(), N * p.misfit_per_pos, nullptr, p.counter.as<unsigned int>(), k_done);
+            PTG_CHECK_LAUNCH();
+            ++p.launches;
+            k_done = k_end;
+        }
+        // complete gradient rows -> complex128 staging -> host
+        const size_t pairs_done = std::min(npairs, (size_t)k_done * chunk);
+        const size_t rows_ready = k_done == kPlaneBlocks ? (size_t)n : (2 * pairs_done) / n;
+        if (rows_ready > rows_out) {
+            const size_t o = rows_out * n, c = (rows_ready - rows_out) * n;
+            dev_to_c128(p.prec, p.stage_out.as<double>() + 2 * o, gd + o, c, p.stream);
+            PTG_CUDA(cudaEventRecord(ev_out[b], p.stream));
+            PTG_CUDA(cudaStreamWaitEvent(p.s_out, ev_out[b], 0));
+            PTG_CUDA(cudaMemcpyAsync(grad + 2 * o, p.stage_out.as<double>() + 2 * o, c * 16, cudaMemcpyDeviceToHost,
+                                     p.s_out));
+            rows_out = rows_ready;
+        }
+    }
+    k_finalize<<<1, 256, 0, p.stream>>>(p.misfit.as<const double>(), N * p.misfit_per_pos, p.dotp.as<const double>(),
+                                        v ? kPlaneBlocks : 0, p.value.as<double>());
+    PTG_CHECK_LAUNCH();
+    ++p.launches;
+    PTG_CUDA(cudaEventRecord(ev_val, p.stream));
+    PTG_CUDA(cudaStreamWaitEvent(p.s_out, ev_val, 0));
+    PTG_CUDA(cudaMemcpyAsync(p.hval.p, p.value.p, sizeof(double), cudaMemcpyDeviceToHost, p.s_out));
+    PTG_CUDA(cudaStreamSynchronize(p.s_out));
+    if (value) *value = *p.hval.as<double>();
+}
+
+void plan_eval_host(Plan& p, int metric, const double* z, const double* v, double* value, double* grad) {
+    LaunchScope ls(p);
+    plan_ensure(p, metric);
+    static const bool off = getenv("PTG_NO_BANDED") && getenv("PTG_NO_BANDED")[0] == '1';   // A/B switch
+    bool sorted = true;
+    for (int j = 1; j < p.N && sorted; ++j) sorted = p.pos_h[2 * j] >= p.pos_h[2 * (j - 1)];
+    const bool banded = !off && grad && p.planes_mode && p.chunks.size() == 1 && !p.mp && !p.timing && sorted &&
+                        p.N > 0 && p.n >= 64;
+    if (banded) {
+        if (p.prec == PTG_C64) eval_host_banded<float>(p, metric, z, v, value, grad);
+        else eval_host_banded<double>(p, metric, z, v, value, grad);
+        return;
+    }
+    const size_t bytes = p.nn() * p.celem();
+    p.zbuf.ensure(bytes);
+    p.gbuf.ensure(bytes);
+    plan_upload_c128(p, z, p.zbuf.p);
+    if (v) {
+        p.vbuf.ensure(bytes);
+        plan_upload_c128(p, v, p.vbuf.p);
+    }
+    plan_eval(p, metric, p.zbuf.p, v ? p.vbuf.p : nullptr, p.gbuf.p, p.value.as<double>());
+    if (grad) plan_download_c128(p, p.gbuf.p, grad);
+    const double val = plan_read_scalar(p, p.value.as<double>());
+    if (value) *value = val;
 }
 
 // --------------------------------------------------------------- simulate

@@ -74,6 +74,10 @@ struct Plan {
 
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
+    // banded host evaluation (plan_eval_host): copy-in / copy-out streams + events
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    std::vector<cudaEvent_t> ev_band;
+    DevMem stage_out;
 
     DevMem pos, probe;
     DevMem amp, inten;               // sqrt(d) and d, real type of the precision
@@ -159,6 +163,9 @@ void plan_ensure(Plan& p, int metric);   // make amp / inten valid for metric
 
 // objective + gradient on device buffers (plan precision); grad may be null
 void plan_eval(Plan& p, int metric, const void* z, const void* v, void* grad, double* value_dev);
+// the same from / to host complex128 buffers (ptg_eval); banded so that the
+// PCIe copies of z in and the gradient out overlap the computation
+void plan_eval_host(Plan& p, int metric, const double* z, const double* v, double* value, double* grad);
 void plan_simulate(Plan& p, const void* z);
 void plan_project(Plan& p, const void* z, int k, void* frame_out);
 // one PIE sweep in place on device object z

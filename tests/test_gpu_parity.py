@@ -247,3 +247,24 @@ def test_ptyf_streamed_upload(tmp_path, oracle):
     b.load_ptyf(path)   # the plan stays usable after failed loads
     vc, gc = b.evaluate(z)
     assert vc == va
+
+
+@pytest.mark.parametrize("cfg_id,with_shift", [(2, False), (2, True), (3, False)])
+def test_banded_host_eval_equals_device_eval(cfg_id, with_shift):
+    """ptg_eval overlaps the PCIe copies with the computation in row bands; the
+    gradient and value are bitwise those of the device-resident evaluation."""
+    import torch
+    from paper_1810_05628_b200 import Plan, synth
+    cfg = synth.CONFIGS[cfg_id]
+    obj, probe, pos = synth.make_inputs(cfg)
+    plan = Plan(cfg.n, cfg.M, cfg.w, pos, None, probe, precision="c64")
+    plan.simulate(obj, copy_out=False)
+    z = obj * 0.9 + 0.05 * rand_field(cfg.n, 11)
+    v = 0.01 * rand_field(cfg.n, 12) if with_shift else None
+    val_h, g_h = plan.evaluate(z, v)
+    zt = torch.from_numpy(z.astype(np.complex64)).cuda()
+    vt = torch.from_numpy(v.astype(np.complex64)).cuda() if v is not None else None
+    gt = torch.empty_like(zt)
+    val_d = plan.evaluate_device(zt, gt, v=vt)
+    assert val_h == val_d
+    assert np.array_equal(g_h, gt.cpu().numpy().astype(np.complex128))
