@@ -12,6 +12,7 @@
 // fused kernel whose four products are read back in a single transfer.
 #include <cooperative_groups.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "solvers.cuh"
@@ -361,6 +362,143 @@ __global__ void __launch_bounds__(kReduceThreads) k_pair_stats(const cplx<T>* nz
     if (threadIdx.x == 0) *reinterpret_cast<unsigned int*>(scratch + 5 * kReduceBlocks) = 0u;
 }
 
+// ------------------------------------------- compact-representation LBFGS
+// For pairs a < A (pointer arrays) and two shared vectors yc, gn:
+//   dot[4a + 0] = <s_a, yc>, dot[4a + 1] = <y_a, yc>, dot[4a + 2] = <s_a, gn>,
+//   dot[4a + 3] = <y_a, gn>,
+// each over k_dot's fixed partition (block x of row r handles pairs 4r..4r+3).
+constexpr int kMdPairs = 4;
+template <typename T>
+struct MultiDotArgs {
+    const cplx<T>* s[kMaxPairs + 1];
+    const cplx<T>* y[kMaxPairs + 1];
+    const cplx<T>* yc;
+    const cplx<T>* gn;
+    int A;
+    size_t len;
+    double* partial;   // [4 A][kReduceBlocks]
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kReduceThreads) k_multi_dot(const MultiDotArgs<T> a) {
+    using C = cplx<T>;
+    __shared__ double red[kMdPairs * 4][kReduceThreads / 32];
+    const size_t chunk = (a.len + kReduceBlocks - 1) / kReduceBlocks;
+    const size_t lo = min(a.len, (size_t)blockIdx.x * chunk), hi = min(a.len, lo + chunk);
+    const int p0 = blockIdx.y * kMdPairs;
+    double acc[kMdPairs * 4];
+#pragma unroll
+    for (int k = 0; k < kMdPairs * 4; ++k) acc[k] = 0.0;
+    for (size_t i = lo + threadIdx.x; i < hi; i += kReduceThreads) {
+        const C yc = a.yc[i], gn = a.gn[i];
+#pragma unroll
+        for (int q = 0; q < kMdPairs; ++q) {
+            if (p0 + q < a.A) {
+                const C sv = a.s[p0 + q][i], yv = a.y[p0 + q][i];
+                acc[4 * q + 0] = __dadd_rn(acc[4 * q + 0], dot_term(sv, yc));
+                acc[4 * q + 1] = __dadd_rn(acc[4 * q + 1], dot_term(yv, yc));
+                acc[4 * q + 2] = __dadd_rn(acc[4 * q + 2], dot_term(sv, gn));
+                acc[4 * q + 3] = __dadd_rn(acc[4 * q + 3], dot_term(yv, gn));
+            }
+        }
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < kMdPairs * 4; ++k) {
+        const double t = warp_tree(acc[k]);
+        if (lane == 0) red[k][w] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < kMdPairs * 4 && p0 + threadIdx.x / 4 < a.A) {
+        double t = 0.0;
+        for (int i = 0; i < kReduceThreads / 32; ++i) t += red[threadIdx.x][i];
+        a.partial[(size_t)(4 * p0 + threadIdx.x) * kReduceBlocks + blockIdx.x] = t;
+    }
+}
+
+// out[d] = k_dot's final tree over partial[d][*], one block per dot
+__global__ void __launch_bounds__(kReduceThreads) k_multi_sum(const double* partial, double* out) {
+    __shared__ double red[kReduceThreads / 32];
+    const double* pd = partial + (size_t)blockIdx.x * kReduceBlocks;
+    double t = 0.0;
+    for (int i = threadIdx.x; i < kReduceBlocks; i += kReduceThreads) t += pd[i];
+    t = warp_tree(t);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double u = 0.0;
+        for (int i = 0; i < kReduceThreads / 32; ++i) u += red[i];
+        out[blockIdx.x] = u;
+    }
+}
+
+// dir = -(gamma g + sum_i u_i s_i + sum_i c_i y_i), accumulated in fp64 per entry
+template <typename T>
+struct CombineArgs {
+    const cplx<T>* s[kMaxPairs];
+    const cplx<T>* y[kMaxPairs];
+    double u[kMaxPairs], c[kMaxPairs];
+    double gamma;
+    int k;
+    const cplx<T>* g;
+    cplx<T>* dir;
+    size_t len;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_combine(const CombineArgs<T> a) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < a.len; i += (size_t)gridDim.x * blockDim.x) {
+        const cplx<T> gv = a.g[i];
+        double rx = a.gamma * (double)gv.x, ry = a.gamma * (double)gv.y;
+        for (int j = 0; j < a.k; ++j) {
+            const cplx<T> sv = a.s[j][i], yv = a.y[j][i];
+            rx = fma(a.u[j], (double)sv.x, fma(a.c[j], (double)yv.x, rx));
+            ry = fma(a.u[j], (double)sv.y, fma(a.c[j], (double)yv.y, ry));
+        }
+        a.dir[i] = mk<T>((T)-rx, (T)-ry);
+    }
+}
+
+template <typename T>
+void multi_dot_t(const Plan& p, const void* const* s, const void* const* y, int A, const void* yc,
+                 const void* gn, double* scratch, double* out_dev) {
+    MultiDotArgs<T> a{};
+    for (int i = 0; i < A; ++i) {
+        a.s[i] = static_cast<const cplx<T>*>(s[i]);
+        a.y[i] = static_cast<const cplx<T>*>(y[i]);
+    }
+    a.yc = static_cast<const cplx<T>*>(yc);
+    a.gn = static_cast<const cplx<T>*>(gn);
+    a.A = A;
+    a.len = p.nn();
+    a.partial = scratch;
+    k_multi_dot<T><<<dim3(kReduceBlocks, (A + kMdPairs - 1) / kMdPairs), kReduceThreads, 0, p.stream>>>(a);
+    k_multi_sum<<<4 * A, kReduceThreads, 0, p.stream>>>(scratch, out_dev);
+    PTG_CHECK_LAUNCH();
+    count_launch(2);
+}
+
+template <typename T>
+void combine_t(const Plan& p, const void* const* s, const void* const* y, const double* u, const double* c,
+               double gamma, int k, const void* g, void* dir) {
+    CombineArgs<T> a{};
+    for (int i = 0; i < k; ++i) {
+        a.s[i] = static_cast<const cplx<T>*>(s[i]);
+        a.y[i] = static_cast<const cplx<T>*>(y[i]);
+        a.u[i] = u[i];
+        a.c[i] = c[i];
+    }
+    a.gamma = gamma;
+    a.k = k;
+    a.g = static_cast<const cplx<T>*>(g);
+    a.dir = static_cast<cplx<T>*>(dir);
+    a.len = p.nn();
+    const int grid = (int)std::min<size_t>(148 * 8, (a.len + 255) / 256);
+    k_combine<T><<<grid, 256, 0, p.stream>>>(a);
+    PTG_CHECK_LAUNCH();
+    count_launch();
+}
+
 template <typename K>
 bool coop_fits(K kern) {
     int dev = 0, sms = 0, per_sm = 0, coop = 0;
@@ -419,6 +557,21 @@ bool dev_two_loop(const Plan& p, const void* const* s, const void* const* y, con
                   const void* g, void* q, double* scratch) {
     return p.prec == PTG_C64 ? launch_two_loop<float>(p, s, y, sy, k, g, q, scratch)
                              : launch_two_loop<double>(p, s, y, sy, k, g, q, scratch);
+}
+
+void dev_multi_dot(const Plan& p, const void* const* s, const void* const* y, int A, const void* yc,
+                   const void* gn, double* scratch, double* out_dev) {
+    if (A <= 0) return;
+    if (A > kMaxPairs + 1) raise(PTG_ERR_INTERNAL, "multi_dot: too many pairs");
+    if (p.prec == PTG_C64) multi_dot_t<float>(p, s, y, A, yc, gn, scratch, out_dev);
+    else multi_dot_t<double>(p, s, y, A, yc, gn, scratch, out_dev);
+}
+
+void dev_combine(const Plan& p, const void* const* s, const void* const* y, const double* u, const double* c,
+                 double gamma, int k, const void* g, void* dir) {
+    if (k > kMaxPairs) raise(PTG_ERR_INTERNAL, "combine: too many pairs");
+    if (p.prec == PTG_C64) combine_t<float>(p, s, y, u, c, gamma, k, g, dir);
+    else combine_t<double>(p, s, y, u, c, gamma, k, g, dir);
 }
 
 void dev_pair_stats(const Plan& p, const void* nz, const void* z, const void* ng, const void* g, void* s_out,

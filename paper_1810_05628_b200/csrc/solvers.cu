@@ -115,24 +115,43 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     const int mem = std::max(0, cfg.lbfgs_memory);
     std::vector<Pair> slots;
     std::deque<int> order;
-    DVec ws;   // fused-kernel scratch (two-loop partials / pair statistics)
+    DVec ws;   // fused-kernel scratch (two-loop partials / pair statistics / products)
     double* wsd = nullptr;
     p.hval.ensure(8 * sizeof(double));
     double* stats_h = p.hval.as<double>() + 2;   // [0] = line-search value
-    // PTG_TWO_LOOP=ops selects the kernel-per-op two-loop (equivalence tests, A/B)
+    // Direction: "compact" (default) — the compact representation of the same
+    // LBFGS matrix (Byrd, Nocedal & Schnabel 1994): the O(k) products it needs
+    // are batched into one pass per iteration and ride on the line search's
+    // synchronisation, the k x k algebra runs on the host, and one combine
+    // pass forms d; "fused" — the reference's two-loop recursion as one
+    // cooperative kernel (bitwise = "ops"); "ops" — one kernel per operation.
     const char* tl = getenv("PTG_TWO_LOOP");
-    bool fused = !(tl && std::string(tl) == "ops");
+    const std::string mode = tl ? std::string(tl) : std::string("compact");
+    bool fused = mode != "ops";
+    const bool compact = mode == "compact" && mem <= kMaxPairs;
+    const int nslot_max = mem + 1;
+    std::vector<double> SY, YY, Sg, Yg;   // by slot id: <s_a, y_b>, <y_a, y_b>, <s_a, g>, <y_a, g>
+    if (compact) {
+        SY.assign((size_t)nslot_max * nslot_max, 0.0);
+        YY.assign((size_t)nslot_max * nslot_max, 0.0);
+        Sg.assign(nslot_max, 0.0);
+        Yg.assign(nslot_max, 0.0);
+    }
+    HostPinned md_h;
+    double gg = g0 * g0;   // <g, g> of the current gradient
     if (satisfied(gnorm)) {
         out.reason = PTG_STOP_TOLERANCE;
     } else {
         ws.s = p.stream;
-        ws.bytes = (size_t)kPairScratch * sizeof(double) + 8 * sizeof(double);
+        ws.bytes = ((size_t)kPairScratch + 8 + (compact ? kMultiDotScratch + 4 * (kMaxPairs + 1) : 0)) * sizeof(double);
         PTG_CUDA(cudaMallocAsync(&ws.p, ws.bytes, p.stream));
         PTG_CUDA(cudaMemsetAsync(ws.p, 0, ws.bytes, p.stream));
         wsd = static_cast<double*>(ws.p);
         double* stats_d = wsd + kPairScratch;
+        double* md_scratch = stats_d + 8;
+        double* md_d = md_scratch + kMultiDotScratch;
+        if (compact) md_h.ensure(4 * (kMaxPairs + 1) * sizeof(double));
         for (int iter = 1; iter <= cfg.max_iters; ++iter) {
-            // direction: fused two-loop + descent check, else the kernel-per-op path
             std::vector<const void*> sp, yp;
             std::vector<double> syv;
             for (int id : order) {
@@ -140,10 +159,46 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                 yp.push_back(slots[id].y.p);
                 syv.push_back(slots[id].sy);
             }
-            fused = fused && dev_two_loop(p, sp.data(), yp.data(), syv.data(), (int)order.size(), g.p, dir.p, wsd);
-            if (!fused) {
-                two_loop(p, sp, yp, syv, g.p, dir.p);
-                if (plan_dot(p, dir.p, g.p, len) >= 0.0) dev_scale(p.prec, dir.p, g.p, -1.0, len, p.stream);
+            const int k = (int)order.size();
+            if (compact) {
+                if (k == 0) {
+                    dev_scale(p.prec, dir.p, g.p, -1.0, len, p.stream);
+                } else {
+                    // H g = gamma g + [S, gamma Y] [[R^-T (D + gamma Y'Y) R^-1, -R^-T], [-R^-1, 0]] [S'g; gamma Y'g]
+                    auto sy = [&](int i, int j) { return SY[(size_t)order[i] * nslot_max + order[j]]; };
+                    auto yy = [&](int i, int j) { return YY[(size_t)order[i] * nslot_max + order[j]]; };
+                    const double gamma = sy(k - 1, k - 1) / yy(k - 1, k - 1);
+                    std::vector<double> t(k), u(k), c(k), rhs(k);
+                    for (int i = k - 1; i >= 0; --i) {   // R t = S'g (R upper triangular)
+                        double a = Sg[order[i]];
+                        for (int j = i + 1; j < k; ++j) a -= sy(i, j) * t[j];
+                        t[i] = a / sy(i, i);
+                    }
+                    for (int i = 0; i < k; ++i) {        // rhs = (D + gamma Y'Y) t - gamma Y'g
+                        double a = sy(i, i) * t[i];
+                        for (int j = 0; j < k; ++j) a += gamma * yy(i, j) * t[j];
+                        rhs[i] = a - gamma * Yg[order[i]];
+                    }
+                    for (int i = 0; i < k; ++i) {        // R' u = rhs
+                        double a = rhs[i];
+                        for (int j = 0; j < i; ++j) a -= sy(j, i) * u[j];
+                        u[i] = a / sy(i, i);
+                    }
+                    double dg = gamma * gg;              // <H g, g>
+                    for (int i = 0; i < k; ++i) {
+                        c[i] = -gamma * t[i];
+                        dg += u[i] * Sg[order[i]] + c[i] * Yg[order[i]];
+                    }
+                    if (-dg >= 0.0) dev_scale(p.prec, dir.p, g.p, -1.0, len, p.stream);   // descent check
+                    else dev_combine(p, sp.data(), yp.data(), u.data(), c.data(), gamma, k, g.p, dir.p);
+                }
+            } else {
+                // fused two-loop + descent check, else the kernel-per-op path
+                fused = fused && dev_two_loop(p, sp.data(), yp.data(), syv.data(), k, g.p, dir.p, wsd);
+                if (!fused) {
+                    two_loop(p, sp, yp, syv, g.p, dir.p);
+                    if (plan_dot(p, dir.p, g.p, len) >= 0.0) dev_scale(p.prec, dir.p, g.p, -1.0, len, p.stream);
+                }
             }
             // candidate pair slot (not in the order deque)
             int slot = -1;
@@ -154,11 +209,20 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                 slot = (int)slots.size() - 1;
             }
             Pair& pr = slots[slot];
-            // pair statistics (+ isFinite of the new iterate) of the accepted point,
+            // pair statistics (+ isFinite of the new iterate) of the accepted point
+            // and, in compact mode, every product the next direction needs,
             // enqueued speculatively behind the first trial's evaluation
+            std::vector<const void*> msp(sp), myp(yp);
+            msp.push_back(pr.s.p);
+            myp.push_back(pr.y.p);
             auto stats = [&]() {
                 dev_pair_stats(p, nz.p, z.p, ng.p, g.p, pr.s.p, pr.y.p, wsd, stats_d);
                 PTG_CUDA(cudaMemcpyAsync(stats_h, stats_d, 5 * sizeof(double), cudaMemcpyDeviceToHost, p.stream));
+                if (compact) {
+                    dev_multi_dot(p, msp.data(), myp.data(), k + 1, pr.y.p, ng.p, md_scratch, md_d);
+                    PTG_CUDA(cudaMemcpyAsync(md_h.p, md_d, 4 * (size_t)(k + 1) * sizeof(double),
+                                             cudaMemcpyDeviceToHost, p.stream));
+                }
             };
             LsOut lsr = d_linesearch(obj, z.p, dir.p, ctr, cfg.linesearch_max, &cur, nz.p, ng.p, stats);
             if (lsr.stalled) {
@@ -171,7 +235,22 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
             }
             if (stats_h[4] != 0.0) raise(PTG_ERR_NUMERIC, "non-finite iterate in lbfgs");
             pr.sy = stats_h[0];
-            if (pr.sy > 1e-12 * std::sqrt(stats_h[1]) * std::sqrt(stats_h[2])) {
+            const bool accept = pr.sy > 1e-12 * std::sqrt(stats_h[1]) * std::sqrt(stats_h[2]);
+            if (compact) {
+                const double* md = md_h.as<double>();
+                for (int a = 0; a <= k; ++a) {
+                    const int sa = a < k ? order[a] : slot;
+                    if (accept) {
+                        SY[(size_t)sa * nslot_max + slot] = md[4 * a];
+                        YY[(size_t)sa * nslot_max + slot] = md[4 * a + 1];
+                        YY[(size_t)slot * nslot_max + sa] = md[4 * a + 1];
+                    }
+                    Sg[sa] = md[4 * a + 2];
+                    Yg[sa] = md[4 * a + 3];
+                }
+                gg = stats_h[3];
+            }
+            if (accept) {
                 order.push_back(slot);
                 if ((int)order.size() > mem) order.pop_front();
             }

@@ -102,6 +102,16 @@ constexpr int kMaxPairs = 64;
 // device cannot co-schedule the grid): use the kernel-per-op path.
 bool dev_two_loop(const Plan& p, const void* const* s, const void* const* y, const double* sy, int k,
                   const void* g, void* q, double* scratch);
+// compact representation (Byrd, Nocedal & Schnabel 1994) of the same LBFGS
+// matrix: 4 products per pair a < A against two shared vectors yc, gn
+// (<s_a,yc>, <y_a,yc>, <s_a,gn>, <y_a,gn> -> out_dev[4a..4a+3]); scratch:
+// 4 (kMaxPairs + 1) kReduceBlocks doubles
+void dev_multi_dot(const Plan& p, const void* const* s, const void* const* y, int A, const void* yc,
+                   const void* gn, double* scratch, double* out_dev);
+// dir = -(gamma g + sum u_i s_i + sum c_i y_i)
+void dev_combine(const Plan& p, const void* const* s, const void* const* y, const double* u, const double* c,
+                 double gamma, int k, const void* g, void* dir);
+constexpr size_t kMultiDotScratch = 4 * (size_t)(kMaxPairs + 1) * kReduceBlocks;
 // s = nz - z, y = ng - g; out_dev[0..4] = <s,y>, <s,s>, <y,y>, <ng,ng>,
 // count of blocks holding a non-finite nz entry.
 // scratch: kPairScratch doubles, zeroed before the first use

@@ -164,6 +164,7 @@ def test_fused_two_loop_matches_per_op(oracle, monkeypatch, precision):
     partition and trees as the kernel-per-op path: identical bits."""
     p, plan, cfg = _patch(oracle, precision)
     z0 = np.ones((cfg.n, cfg.n), np.complex128)
+    monkeypatch.setenv("PTG_TWO_LOOP", "fused")
     a = plan.lbfgs(z0, max_iters=30, lbfgs_memory=5)
     monkeypatch.setenv("PTG_TWO_LOOP", "ops")
     b = plan.lbfgs(z0, max_iters=30, lbfgs_memory=5)
@@ -202,3 +203,16 @@ def test_truncated_newton_c64_descends(oracle):
     vals = r.history[:, 1]
     assert np.all(np.diff(vals) <= 0) and vals[-1] < vals[0]
     assert r.weighted_evals == r.history[-1, 0]
+
+
+def test_compact_lbfgs_matches_two_loop(oracle, monkeypatch):
+    """The compact representation (default) is the same LBFGS matrix as the
+    reference's two-loop recursion: c128 trajectories agree to rounding."""
+    p, plan, cfg = _patch(oracle, "c128")
+    z0 = np.ones((cfg.n, cfg.n), np.complex128)
+    a = plan.lbfgs(z0, max_iters=25, lbfgs_memory=5)
+    monkeypatch.setenv("PTG_TWO_LOOP", "fused")
+    b = plan.lbfgs(z0, max_iters=25, lbfgs_memory=5)
+    assert a.weighted_evals == b.weighted_evals and a.reason == b.reason
+    np.testing.assert_allclose(a.history, b.history, rtol=1e-10)
+    assert rel_l2(a.final_iterate, b.final_iterate) <= 1e-10
