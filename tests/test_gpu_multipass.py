@@ -81,3 +81,27 @@ def test_m256_mgopt_values(oracle):
     got = Hierarchy(plan, 2).driver(z0, budget=1e9, max_cycles=1)
     assert got.history.shape == want.history.shape
     np.testing.assert_allclose(got.history[:, 1], want.history[:, 1], rtol=1e-4)
+
+
+@pytest.mark.parametrize("M", [128, 256])
+@pytest.mark.parametrize("with_probe", [True, False])
+@pytest.mark.parametrize("metric", [0, 1])
+def test_cluster_kernel_c64(oracle, M, with_probe, metric):
+    """complex64 M = 128 / 256 run the cluster-split kernel (csrc/frame_cl.cuh):
+    complex probe or binary window, both metrics, jittered (odd) positions."""
+    from paper_1810_05628_b200 import Plan, synth
+    n = 2 * M + 8
+    cfg = synth.Config(0, n, M, 3, M // 2 + 3, 8.0, M / 4, 0.0006, "c64", jitter=2)
+    obj, probe, pos = synth.make_inputs(cfg)
+    probe = probe if with_probe else None
+    z = obj * 0.9 + 0.05 * rand_field(n, 6)
+    obj, z = obj.astype(np.complex64).astype(np.complex128), z.astype(np.complex64).astype(np.complex128)
+    if probe is not None:
+        probe = probe.astype(np.complex64).astype(np.complex128)
+    data = oracle.simulate(n, M, M, pos, obj, probe).astype(np.float32)
+    p = oracle.Problem(n, M, M, pos, data.astype(np.float64), probe, metric)
+    plan = Plan(n, M, M, pos, data, probe, precision="c64")
+    wv, wg = oracle.evaluate(p, z)
+    gv, gg = plan.evaluate(z, metric=metric)
+    assert rel(gv, wv) <= 1e-5
+    assert rel_l2(gg, wg) <= 1e-4
