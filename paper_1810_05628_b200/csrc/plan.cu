@@ -21,6 +21,7 @@
 #include "frame_kernels.cuh"
 #include "frame_multipass.cuh"
 #include "frame_tma.cuh"
+#include "pie_reg.cuh"
 #include "plan.cuh"
 #include "transfer.cuh"
 
@@ -713,8 +714,32 @@ void launch_pie_t(Plan& p, void* z, const void* wgt, double damping) {
     ++p.launches;
 }
 
+template <int M>
+void launch_pie_reg(Plan& p, void* z, const void* wgt, double damping) {
+    constexpr size_t smem = pie_reg_smem_bytes<M>();
+    static bool attr = false;
+    if (!attr) {
+        PTG_CUDA(cudaFuncSetAttribute(k_pie_reg<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    k_pie_reg<M><<<1, M, smem, p.stream>>>(static_cast<float2*>(z), p.has_probe ? p.probe.as<const float2>() : nullptr,
+                                          p.pos.as<const int2>(), p.amp.as<const float>(), p.N, p.n,
+                                          static_cast<const float2*>(wgt), (float)damping);
+    PTG_CHECK_LAUNCH();
+    ++p.launches;
+}
+
 template <typename T>
 void launch_pie(Plan& p, void* z, const void* wgt, double damping) {
+    static const bool generic = getenv("PTG_PIE_GENERIC") && getenv("PTG_PIE_GENERIC")[0] == '1';   // A/B switch
+    if constexpr (sizeof(T) == 4) {
+        if (!generic && p.w == p.M && (p.M == 16 || p.M == 32 || p.M == 64)) {
+            if (p.M == 16) launch_pie_reg<16>(p, z, wgt, damping);
+            else if (p.M == 32) launch_pie_reg<32>(p, z, wgt, damping);
+            else launch_pie_reg<64>(p, z, wgt, damping);
+            return;
+        }
+    }
     switch (p.M) {
         case 1: launch_pie_t<T, 1>(p, z, wgt, damping); break;
         case 2: launch_pie_t<T, 2>(p, z, wgt, damping); break;
