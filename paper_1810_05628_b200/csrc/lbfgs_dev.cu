@@ -300,8 +300,9 @@ __global__ void __launch_bounds__(kTlThreads, 1) k_two_loop(const TwoLoopArgs<T>
     }
 }
 
-// s = nz - z, y = ng - g and <s,y>, <s,s>, <y,y>, <ng,ng> over k_dot's
-// partition, plus the isFinite test of nz (ComplexField::isFinite)
+// s = nz - z, y = ng - g and <s,y>, <s,s>, <y,y>, <ng,ng> over a fixed
+// partition of kPsBlocks blocks, plus the isFinite test of nz (ComplexField::isFinite)
+constexpr int kPsBlocks = 296;
 template <typename T>
 __global__ void __launch_bounds__(kReduceThreads) k_pair_stats(const cplx<T>* nz, const cplx<T>* z,
                                                                const cplx<T>* ng, const cplx<T>* g,
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_pair_stats(const cplx<T>* nz
                                                                double* scratch, double* out) {
     __shared__ double red[4][kReduceThreads / 32];
     __shared__ bool last;
-    const size_t chunk = (len + kReduceBlocks - 1) / kReduceBlocks;
+    const size_t chunk = (len + kPsBlocks - 1) / kPsBlocks;
     const size_t lo = min(len, (size_t)blockIdx.x * chunk), hi = min(len, lo + chunk);
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     bool bad = false;
@@ -341,14 +342,14 @@ __global__ void __launch_bounds__(kReduceThreads) k_pair_stats(const cplx<T>* nz
     if (threadIdx.x == 0) {
         __threadfence();
         unsigned int* ctr = reinterpret_cast<unsigned int*>(scratch + 5 * kReduceBlocks);
-        last = atomicAdd(ctr, 1u) == kReduceBlocks - 1;
+        last = atomicAdd(ctr, 1u) == kPsBlocks - 1;
     }
     __syncthreads();
     if (!last) return;
     __threadfence();
     for (int q = 0; q < 5; ++q) {
         double t = 0.0;
-        for (int i = threadIdx.x; i < kReduceBlocks; i += kReduceThreads) t += __ldcg(scratch + q * kReduceBlocks + i);
+        for (int i = threadIdx.x; i < kPsBlocks; i += kReduceThreads) t += __ldcg(scratch + q * kReduceBlocks + i);
         t = warp_tree(t);
         __syncthreads();
         if (lane == 0) red[0][w] = t;
@@ -368,6 +369,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_pair_stats(const cplx<T>* nz
 //   dot[4a + 3] = <y_a, gn>,
 // each over k_dot's fixed partition (block x of row r handles pairs 4r..4r+3).
 constexpr int kMdPairs = 4;
+constexpr int kMdBlocks = 148;   // partition of the batched products (one tree per block and product)
 template <typename T>
 struct MultiDotArgs {
     const cplx<T>* s[kMaxPairs + 1];
@@ -376,14 +378,14 @@ struct MultiDotArgs {
     const cplx<T>* gn;
     int A;
     size_t len;
-    double* partial;   // [4 A][kReduceBlocks]
+    double* partial;   // [4 A][kMdBlocks]
 };
 
 template <typename T>
 __global__ void __launch_bounds__(kReduceThreads) k_multi_dot(const MultiDotArgs<T> a) {
     using C = cplx<T>;
     __shared__ double red[kMdPairs * 4][kReduceThreads / 32];
-    const size_t chunk = (a.len + kReduceBlocks - 1) / kReduceBlocks;
+    const size_t chunk = (a.len + kMdBlocks - 1) / kMdBlocks;
     const size_t lo = min(a.len, (size_t)blockIdx.x * chunk), hi = min(a.len, lo + chunk);
     const int p0 = blockIdx.y * kMdPairs;
     double acc[kMdPairs * 4];
@@ -412,16 +414,16 @@ __global__ void __launch_bounds__(kReduceThreads) k_multi_dot(const MultiDotArgs
     if (threadIdx.x < kMdPairs * 4 && p0 + threadIdx.x / 4 < a.A) {
         double t = 0.0;
         for (int i = 0; i < kReduceThreads / 32; ++i) t += red[threadIdx.x][i];
-        a.partial[(size_t)(4 * p0 + threadIdx.x) * kReduceBlocks + blockIdx.x] = t;
+        a.partial[(size_t)(4 * p0 + threadIdx.x) * kMdBlocks + blockIdx.x] = t;
     }
 }
 
-// out[d] = k_dot's final tree over partial[d][*], one block per dot
+// out[d] = fixed tree over partial[d][*], one block per product
 __global__ void __launch_bounds__(kReduceThreads) k_multi_sum(const double* partial, double* out) {
     __shared__ double red[kReduceThreads / 32];
-    const double* pd = partial + (size_t)blockIdx.x * kReduceBlocks;
+    const double* pd = partial + (size_t)blockIdx.x * kMdBlocks;
     double t = 0.0;
-    for (int i = threadIdx.x; i < kReduceBlocks; i += kReduceThreads) t += pd[i];
+    for (int i = threadIdx.x; i < kMdBlocks; i += kReduceThreads) t += pd[i];
     t = warp_tree(t);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
     __syncthreads();
@@ -450,10 +452,22 @@ __global__ void __launch_bounds__(256) k_combine(const CombineArgs<T> a) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < a.len; i += (size_t)gridDim.x * blockDim.x) {
         const cplx<T> gv = a.g[i];
         double rx = a.gamma * (double)gv.x, ry = a.gamma * (double)gv.y;
-        for (int j = 0; j < a.k; ++j) {
-            const cplx<T> sv = a.s[j][i], yv = a.y[j][i];
-            rx = fma(a.u[j], (double)sv.x, fma(a.c[j], (double)yv.x, rx));
-            ry = fma(a.u[j], (double)sv.y, fma(a.c[j], (double)yv.y, ry));
+        constexpr int U = 8;   // loads of U pairs in flight together
+        for (int j0 = 0; j0 < a.k; j0 += U) {
+            cplx<T> sv[U], yv[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                if (j0 + q < a.k) {
+                    sv[q] = a.s[j0 + q][i];
+                    yv[q] = a.y[j0 + q][i];
+                }
+#pragma unroll
+            for (int q = 0; q < U; ++q)
+                if (j0 + q < a.k) {
+                    const int j = j0 + q;
+                    rx = fma(a.u[j], (double)sv[q].x, fma(a.c[j], (double)yv[q].x, rx));
+                    ry = fma(a.u[j], (double)sv[q].y, fma(a.c[j], (double)yv[q].y, ry));
+                }
         }
         a.dir[i] = mk<T>((T)-rx, (T)-ry);
     }
@@ -472,7 +486,7 @@ void multi_dot_t(const Plan& p, const void* const* s, const void* const* y, int 
     a.A = A;
     a.len = p.nn();
     a.partial = scratch;
-    k_multi_dot<T><<<dim3(kReduceBlocks, (A + kMdPairs - 1) / kMdPairs), kReduceThreads, 0, p.stream>>>(a);
+    k_multi_dot<T><<<dim3(kMdBlocks, (A + kMdPairs - 1) / kMdPairs), kReduceThreads, 0, p.stream>>>(a);
     k_multi_sum<<<4 * A, kReduceThreads, 0, p.stream>>>(scratch, out_dev);
     PTG_CHECK_LAUNCH();
     count_launch(2);
@@ -578,11 +592,11 @@ void dev_pair_stats(const Plan& p, const void* nz, const void* z, const void* ng
                     void* y_out, double* scratch, double* out_dev) {
     const size_t len = p.nn();
     if (p.prec == PTG_C64)
-        k_pair_stats<float><<<kReduceBlocks, kReduceThreads, 0, p.stream>>>(
+        k_pair_stats<float><<<kPsBlocks, kReduceThreads, 0, p.stream>>>(
             (const float2*)nz, (const float2*)z, (const float2*)ng, (const float2*)g, (float2*)s_out, (float2*)y_out,
             len, scratch, out_dev);
     else
-        k_pair_stats<double><<<kReduceBlocks, kReduceThreads, 0, p.stream>>>(
+        k_pair_stats<double><<<kPsBlocks, kReduceThreads, 0, p.stream>>>(
             (const double2*)nz, (const double2*)z, (const double2*)ng, (const double2*)g, (double2*)s_out,
             (double2*)y_out, len, scratch, out_dev);
     PTG_CHECK_LAUNCH();

@@ -383,7 +383,9 @@ __device__ __forceinline__ void finalize_block(const double* misfit, int N, cons
 constexpr int kPlaneBlocks = 148 * 4;   // fixed grid => fixed dot partition (deterministic)
 // grad = sum_c planes[c] (fixed colour order) - v, <v,z> partials, fused final
 // value (last block).  Pure streaming: every thread owns a fixed pixel pair.
-template <typename T>
+// QS lanes per pixel pair (small problems: more loads in flight per pair);
+// lane q sums colours q, q + QS, ... in order, lanes combine by a fixed xor tree
+template <typename T, int QS>
 __global__ void __launch_bounds__(256) k_plane_reduce(const cplx<T>* __restrict__ planes, int ncol, size_t nn,
                                                       const cplx<T>* __restrict__ v, const cplx<T>* __restrict__ z,
                                                       cplx<T>* __restrict__ grad, double* __restrict__ dotp,
@@ -396,23 +398,25 @@ __global__ void __launch_bounds__(256) k_plane_reduce(const cplx<T>* __restrict_
     __shared__ double red[8];
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int lin = threadIdx.x;
+    const int q = lin % QS;
+    const unsigned gmask = QS == 1 ? 0u : (((1u << QS) - 1u) << ((lin & 31) & ~(QS - 1)));
     const int b = block0 + blockIdx.x;
     const size_t npairs = (nn + 1) / 2;
     const size_t chunk = (npairs + kPlaneBlocks - 1) / kPlaneBlocks;
     const size_t lo = min(npairs, b * chunk), hi = min(lo + chunk, npairs);
     double d = 0.0;
-    for (size_t pr = lo + lin; pr < hi; pr += blockDim.x) {
+    for (size_t pr = lo + lin / QS; pr < hi; pr += blockDim.x / QS) {
         const size_t i = 2 * pr;
         const bool two = i + 1 < nn;
         cplx<T> a0 = mk<T>(T(0), T(0)), a1 = a0;
         constexpr int B = 8;
-        for (int c0 = 0; c0 < ncol; c0 += B) {
+        for (int c0 = q; c0 < ncol; c0 += B * QS) {
             cplx<T> q0[B], q1[B];
 #pragma unroll
             for (int u = 0; u < B; ++u) {
                 q0[u] = q1[u] = mk<T>(T(0), T(0));
-                if (c0 + u < ncol) {
-                    const cplx<T>* s = planes + (size_t)(c0 + u) * nn + i;
+                if (c0 + u * QS < ncol) {
+                    const cplx<T>* s = planes + (size_t)(c0 + u * QS) * nn + i;
                     if constexpr (sizeof(T) == 4) {
                         if (two && (nn % 2 == 0)) {   // 16-B aligned pair
                             const float4 f = __ldg(reinterpret_cast<const float4*>(s));
@@ -433,6 +437,14 @@ __global__ void __launch_bounds__(256) k_plane_reduce(const cplx<T>* __restrict_
                 a0 = cadd(a0, q0[u]);
                 a1 = cadd(a1, q1[u]);
             }
+        }
+        if constexpr (QS > 1) {
+#pragma unroll
+            for (int o = 1; o < QS; o <<= 1) {
+                a0 = cadd(a0, mk<T>(__shfl_xor_sync(gmask, a0.x, o), __shfl_xor_sync(gmask, a0.y, o)));
+                a1 = cadd(a1, mk<T>(__shfl_xor_sync(gmask, a1.x, o), __shfl_xor_sync(gmask, a1.y, o)));
+            }
+            if (q != 0) continue;
         }
         if (v) {
             const cplx<T> v0 = v[i], z0 = z[i];
@@ -468,6 +480,17 @@ __global__ void __launch_bounds__(256) k_plane_reduce(const cplx<T>* __restrict_
         finalize_block(misfit, N, dotp, gridDim.x, value_out, red, lin);
         if (lin == 0) *counter = 0u;
     }
+}
+
+// lanes per pixel pair of the plane reduce: the fixed partition gives each block
+// `chunk` pairs; small planes (coarse MG levels) split a pair's colours over lanes
+inline int plane_qs(const Plan& p) {
+    const size_t chunk = ((p.nn() + 1) / 2 + kPlaneBlocks - 1) / kPlaneBlocks;
+    return chunk <= 64 ? 4 : chunk <= 128 ? 2 : 1;
+}
+template <typename T>
+auto plane_reduce_kernel(int qs) {
+    return qs == 4 ? k_plane_reduce<T, 4> : qs == 2 ? k_plane_reduce<T, 2> : k_plane_reduce<T, 1>;
 }
 
 // --------------------------------------------------------- overlap gather
@@ -1135,7 +1158,7 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
             cfg.attrs = attr;
             cfg.numAttrs = p.timing ? 0 : 1;
             p.ev_begin(1);
-            PTG_CUDA(cudaLaunchKernelEx(&cfg, k_plane_reduce<T>, p.planes.as<const C>(), p.ncolors, p.nn(),
+            PTG_CUDA(cudaLaunchKernelEx(&cfg, plane_reduce_kernel<T>(plane_qs(p)), p.planes.as<const C>(), p.ncolors, p.nn(),
                                         static_cast<const C*>(v), static_cast<const C*>(z), static_cast<C*>(grad),
                                         p.dotp.as<double>(), p.misfit.as<const double>(), p.N * p.misfit_per_pos,
                                         value_dev, p.counter.as<unsigned int>(), 0));
@@ -1283,7 +1306,7 @@ static void eval_host_banded(Plan& p, int metric, const double* z, const double*
             ++k_end;
         }
         if (k_end > k_done) {
-            k_plane_reduce<T><<<k_end - k_done, 256, 0, p.stream>>>(
+            plane_reduce_kernel<T>(plane_qs(p))<<<k_end - k_done, 256, 0, p.stream>>>(
                 p.planes.as<const C>(), p.ncolors, nn, vd, zd, gd, p.dotp.as<double>(),
                 p.misfit.as<const double>(), N * p.misfit_per_pos, nullptr, p.counter.as<unsigned int>(), k_done);
             PTG_CHECK_LAUNCH();
