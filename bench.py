@@ -305,7 +305,11 @@ def run_ours(args):
     # roofline of the dominant kernel (frame kernel), live CUDA-event durations
     peaks, peak_src = load_peaks()
     B, F = algorithmic(cfg, Nr)
-    avg_frame_s = (frame_ms / max(frame_n, 1)) / 1e3
+    # per evaluation: a large problem launches the frame kernel once per stash
+    # chunk, so the algorithmic work of one evaluation is set against the
+    # summed duration of its launches (= per-launch work / per-launch time)
+    launches_per_eval = max(frame_n, 1) / max(args.steps, 1)
+    avg_frame_s = (frame_ms / max(args.steps, 1)) / 1e3
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved_gbs = B / avg_frame_s / 1e9
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
@@ -315,10 +319,11 @@ def run_ours(args):
     roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved_gbs / hbm_peak, "traffic": traffic,
                 "kernel": f"frame_kernel<float,{cfg.M}> (one CTA per scan position)",
-                "algorithmic_bytes_per_launch": B, "avg_launch_us": avg_frame_s * 1e6,
+                "algorithmic_bytes_per_launch": B / launches_per_eval,
+                "avg_launch_us": avg_frame_s * 1e6 / launches_per_eval, "launches_per_eval": launches_per_eval,
                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"}
     roofline_fp32 = {"bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
-                     "frac": achieved_tf / fp32_peak, "algorithmic_flops_per_launch": F,
+                     "frac": achieved_tf / fp32_peak, "algorithmic_flops_per_launch": F / launches_per_eval,
                      "convention": "F(M)=10 M^2 log2(M^2) + 24 M^2 per pattern (SURVEY 8d)",
                      "peak_source": f"nominal 148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (no measured FP32 figure)"}
     eval_share = {"frame_kernel_ms": frame_ms / max(args.steps, 1), "gather_ms": gather_ms / max(args.steps, 1),
