@@ -9,10 +9,15 @@ all 841 patterns; metric = diffraction patterns per second.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
 
-Multi-GPU (torchrun, one rank per GPU): scan rows are split contiguously over
-ranks (weak in patterns per rank, fixed total = strong on the eval); each rank
-evaluates its shard and the gradient + misfit are summed with NCCL allreduce
-(the path's one real exchange step).
+Multi-GPU (torchrun, one rank per GPU), default --scaling weak: band
+decomposition of one scanned object — rank r owns the config-2
+problem on an n x n band of a tall object whose bands overlap by w - step
+rows (the scan continues across bands); each rank evaluates its band, the
+shared gradient rows are summed with the neighbours (NCCL point-to-point, the
+path's real exchange step) and the misfit with a scalar allreduce.  Per-GPU
+work is fixed; value = all ranks' patterns per second.  --scaling strong:
+config 2's scan rows split over ranks with the object replicated and the full
+gradient allreduced (north_star's baseline layout).
 
 --impl reference: the reference's own CPU path on the host cores (rank 0
 only): the patch-model restatement over the reference's compiled OpenMP
@@ -50,6 +55,8 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-extras", action="store_true", help="skip V-cycle / PIE / CPU legs")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="multi-GPU layout: weak = object bands + halo exchange, strong = replicated object + allreduce")
     return ap.parse_args()
 
 
@@ -228,11 +235,24 @@ def run_ours(args):
 
     from paper_1810_05628_b200 import Hierarchy, Plan, synth
 
+    from paper_1810_05628_b200 import sharding
+
     cfg = synth.CONFIGS[args.config]
     obj, probe, pos = synth.make_inputs(cfg)
-    rows_per = -(-cfg.steps // world)
-    lo, hi = min(rank * rows_per, cfg.steps) * cfg.steps, min((rank + 1) * rows_per, cfg.steps) * cfg.steps
-    pos_shard = pos[lo:hi]
+    banded = world > 1 and args.scaling == "weak"
+    overlap = cfg.w - cfg.step if banded else 0
+    if banded:
+        # rank r: the config's scan on rows [r (n - overlap), + n) of a tall object
+        H = world * (cfg.n - overlap) + overlap
+        off = sharding.band_offset(rank, cfg.n, overlap)
+        big = synth.make_object(H, cfg.sigma_obj)
+        obj = np.ascontiguousarray(big[off:off + cfg.n, :cfg.n])
+        del big
+        pos_shard = pos
+    else:
+        rows_per = -(-cfg.steps // world)
+        lo, hi = min(rank * rows_per, cfg.steps) * cfg.steps, min((rank + 1) * rows_per, cfg.steps) * cfg.steps
+        pos_shard = pos[lo:hi]
     Nr = pos_shard.shape[0]
 
     cdt = torch.complex64 if cfg.precision == "c64" else torch.complex128
@@ -253,11 +273,18 @@ def run_ours(args):
     flush = torch.ones(128 << 20, dtype=torch.float32, device="cuda")
     flush_out = torch.empty(1, dtype=torch.float32, device="cuda")
 
+    def exchange(g, v):
+        if dist is None:
+            return
+        if banded:
+            sharding.halo_exchange(g, overlap)   # shared band rows with the neighbours
+        else:
+            dist.all_reduce(torch.view_as_real(g))
+        dist.all_reduce(v[:1])
+
     def step():
         plan.evaluate_device(z, grad, value_dev=val, sync_value=False)
-        if dist is not None:
-            dist.all_reduce(torch.view_as_real(grad))
-            dist.all_reduce(val[:1])
+        exchange(grad, val)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -298,7 +325,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms = float(t.item())
 
-    total_patterns = cfg.N
+    total_patterns = cfg.N * world if banded else cfg.N
     value = total_patterns * args.steps / (t_ms / 1e3)
     ms_per_step = t_ms / args.steps
 
@@ -352,8 +379,7 @@ def run_ours(args):
         for _ in range(args.steps):
             zt.copy_(torch.from_numpy(zh).to(cdt), non_blocking=False)
             plan.evaluate_device(zt, grad, value_dev=val, sync_value=False)
-            dist.all_reduce(torch.view_as_real(grad))
-            dist.all_reduce(val[:1])
+            exchange(grad, val)
             torch.from_numpy(gh).copy_(grad.to(torch.complex128))
             float(val[0].item())
         e2e_s = time.perf_counter() - t0
@@ -421,10 +447,16 @@ def run_ours(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f32" if cfg.precision == "c64" else "f64",
+                "scaling": "weak" if banded else "strong", "vs_baseline": None,
+                "dtype": "f32" if cfg.precision == "c64" else "f64",
                 "data": "synthetic (seeded smooth object, Gaussian x quadratic-phase probe, data by our GPU forward operator)",
-                "config": {"workload": cfg.describe(), "global_batch": cfg.N, "patterns_per_rank": Nr,
-                           "parallelism": f"scan-row sharding x{world} + NCCL allreduce" if world > 1 else "single GPU",
+                "config": {"workload": cfg.describe() if not banded else
+                           (f"{cfg.describe()} per GPU: {world} bands of a {world * (cfg.n - overlap) + overlap}x{cfg.n} "
+                            f"object, consecutive bands sharing {overlap} rows (one continuous raster)"),
+                           "global_batch": total_patterns, "patterns_per_rank": Nr,
+                           "parallelism": (f"object bands x{world} + NCCL halo exchange ({overlap} rows) + scalar allreduce"
+                                           if banded else f"scan-row sharding x{world} + NCCL allreduce")
+                           if world > 1 else "single GPU",
                            "l2": "flushed between timed steps (512 MiB read)"},
                 "roofline": roofline, "roofline_fp32": roofline_fp32, "step_breakdown": eval_share,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks}

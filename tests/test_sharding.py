@@ -66,3 +66,55 @@ def test_two_rank_allreduce_matches_single_process():
     val, full_val, grad_rel, span = q.get(timeout=5)
     assert abs(val - full_val) <= 1e-12 * abs(full_val)
     assert grad_rel <= 1e-12
+
+
+def _band_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import ptgo
+        from paper_1810_05628_b200 import sharding, synth
+        nb, M, s = 40, 16, 8                 # band side, frame, stride
+        ov = M - s                           # rows shared by consecutive bands' scans
+        H = world * (nb - ov) + ov           # global rows; the scan uses columns [0, nb)
+        obj = synth.make_object(H, 2.0)
+        probe = synth.make_probe(M, 4.0, 0.01)
+        loc = np.array([[r, c] for r in range(0, nb - M + 1, s) for c in range(0, nb - M + 1, s)], np.int32)
+        glob = np.concatenate([loc + [sharding.band_offset(b, nb, ov), 0] for b in range(world)])
+        data = ptgo.simulate(H, M, M, glob, obj, probe)
+        z = obj * 0.9 + 0.05
+        off = sharding.band_offset(rank, nb, ov)
+        k = loc.shape[0]
+        band = np.ascontiguousarray(z[off:off + nb, :nb])
+        val, g = ptgo.evaluate(ptgo.Problem(nb, M, M, loc, data[rank * k:(rank + 1) * k], probe), band)
+        gt = torch.from_numpy(g.copy())
+        sharding.halo_exchange(gt, ov)
+        val = sharding.allreduce_value(val)
+        full_val, full_g = ptgo.evaluate(ptgo.Problem(H, M, M, glob, data, probe), z)
+        want = full_g[off:off + nb, :nb]
+        q.put((rank, val, full_val, float(np.linalg.norm(gt.numpy() - want) / np.linalg.norm(want))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+@pytest.mark.parametrize("world", [2, 3])
+def test_band_decomposition_matches_global_object(world):
+    """Weak-scaling layout: each rank evaluates its own band; halo rows summed
+    point-to-point with the neighbours reproduce the global gradient."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_band_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(150)
+    assert all(p.exitcode == 0 for p in ps)
+    for _ in range(world):
+        rank, val, full_val, grad_rel = q.get(timeout=5)
+        assert abs(val - full_val) <= 1e-12 * abs(full_val)
+        assert grad_rel <= 1e-12
