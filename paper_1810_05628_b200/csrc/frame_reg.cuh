@@ -88,6 +88,12 @@ __device__ __forceinline__ float2 epi_contrib(float2 x, float2 P, float sc) {
     return make_float2(fmaf(P.x, a, -(P.y * b)), fmaf(-P.x, b, -(P.y * a)));
 }
 __device__ __forceinline__ float2 epi_contrib(float2 x, float sc) { return make_float2(x.x * sc, -x.y * sc); }
+// the same with a pre-scaled, pre-conjugated probe Pc = conj(sc * P):
+// conj(sc P x) = Pc * conj(x) = cmul((x.x, -x.y), Pc) -- the conj lands on the
+// broadcast scalar, so the product is one FMUL2 + one FFMA2
+__device__ __forceinline__ float2 epi_contrib_pre(float2 x, float2 Pc) {
+    return cmul(make_float2(x.x, -x.y), Pc);
+}
 
 // ------------------------------------------------------ register line FFT
 // Compile-time twiddles: Taylor series evaluated by the compiler (constexpr),

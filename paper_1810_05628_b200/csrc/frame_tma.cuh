@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
     }
     // let the dependent gather kernel start launching (it waits on griddepcontrol.wait)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    // epilogue: contribution = sc * conj(P) o IDFT_u(R) = sc * conj(P o conj(x))
+    // epilogue: contribution = sc * conj(P) o IDFT_u(R) = conj(sc P) o conj(x)
     if (live) {
         // stash row pitch M + 2, window row at offset (col0 & 1), zero pads (plan.cuh)
         const float sc = (OP == OP_DISTANCE) ? 1.f / (float(M) * float(M)) : 2.f;
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
             float2* __restrict__ pl = a.planes + (size_t)a.color[j] * a.n * a.n + (size_t)pj.x * a.n + pj.y + t;
 #pragma unroll
             for (int r = 0; r < M; ++r) {
-                const float2 v = PROBE ? epi_contrib(x[r], buf[r * M + t], sc) : epi_contrib(x[r], sc);
+                const float2 v = PROBE ? epi_contrib_pre(x[r], buf[r * M + t]) : epi_contrib(x[r], sc);
                 pl[(size_t)r * a.n] = v;
             }
             return;
@@ -244,8 +244,8 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
         float2* __restrict__ out = a.stash + (size_t)j * M * S;
 #pragma unroll
         for (int r = 0; r < M; ++r) {
-            // probe tile (dense pitch M)
-            const float2 v = PROBE ? epi_contrib(x[r], buf[r * M + t], sc) : epi_contrib(x[r], sc);
+            // pre-scaled conjugated probe tile conj(sc * P) (dense pitch M)
+            const float2 v = PROBE ? epi_contrib_pre(x[r], buf[r * M + t]) : epi_contrib(x[r], sc);
             out[(size_t)r * S + odd + t] = v;
         }
         // the two zero pads of row t

@@ -162,6 +162,12 @@ void encode_amp(CUtensorMap* tm, const void* amp, int M, int N) {
     if (r != CUDA_SUCCESS) raise(PTG_ERR_CUDA, "tensor map (data) encode failed: " + std::to_string((int)r));
 }
 
+// conj(sc * P) for the complex64 TMA epilogue
+__global__ void k_scale_conj_c64(float2* __restrict__ out, const float2* __restrict__ in, float sc, size_t n) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = make_float2(in[i].x * sc, -(in[i].y * sc));
+}
+
 bool tma_path_ok(const Plan& p) {
     return p.prec == PTG_C64 && (p.M == 16 || p.M == 32 || p.M == 64) && p.w == p.M && p.n % 2 == 0 &&
            p.N > 0;
@@ -200,11 +206,22 @@ void launch_tma(Plan& p, const FrameArgs<float>& a, int count, const void* z, co
     }
     const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(p.tm_amp);
     const bool pr = a.probe != nullptr;
-    if (pr && !p.tm_probe_ok) {   // probe M x M complex64 as float32 [M][2M], one box
-        encode_z(reinterpret_cast<CUtensorMap*>(p.tm_probe), a.probe, p.M, p.M, 0);
+    if (pr && !p.tm_probe_ok) {
+        // the epilogue reads conj(sc * P) (sc = 1/M^2 distance, 2 intensity:
+        // powers of two, so the table is exact): M x M complex64 as float32 [M][2M], one box
+        p.probe_epi.alloc(2 * p.MM() * sizeof(float2));
+        float2* pe = p.probe_epi.as<float2>();
+        const float sc[2] = {1.f / ((float)p.M * (float)p.M), 2.f};
+        for (int k = 0; k < 2; ++k) {
+            k_scale_conj_c64<<<(unsigned)((p.MM() + 255) / 256), 256, 0, p.stream>>>(
+                pe + k * p.MM(), p.probe.as<const float2>(), sc[k], p.MM());
+            PTG_CHECK_LAUNCH();
+            encode_z(reinterpret_cast<CUtensorMap*>(p.tm_probe_epi[k]), pe + k * p.MM(), p.M, p.M, 0);
+        }
         p.tm_probe_ok = true;
     }
-    const CUtensorMap& tp = pr ? *reinterpret_cast<const CUtensorMap*>(p.tm_probe) : *tz;
+    const CUtensorMap& tp =
+        pr ? *reinterpret_cast<const CUtensorMap*>(p.tm_probe_epi[OP == OP_INTENSITY ? 1 : 0]) : *tz;
     switch (p.M) {
         case 16: pr ? launch_tma_p<16, OP, true>(a, count, *tz, ta, tp, p.stream) : launch_tma_p<16, OP, false>(a, count, *tz, ta, tp, p.stream); break;
         case 32: pr ? launch_tma_p<32, OP, true>(a, count, *tz, ta, tp, p.stream) : launch_tma_p<32, OP, false>(a, count, *tz, ta, tp, p.stream); break;
@@ -386,7 +403,7 @@ constexpr int kPlaneBlocks = 148 * 4;   // fixed grid => fixed dot partition (de
 // QS lanes per pixel pair (small problems: more loads in flight per pair);
 // lane q sums colours q, q + QS, ... in order, lanes combine by a fixed xor tree
 template <typename T, int QS>
-__global__ void __launch_bounds__(256) k_plane_reduce(const cplx<T>* __restrict__ planes, int ncol, size_t nn,
+__global__ void __launch_bounds__(256, 4) k_plane_reduce(const cplx<T>* __restrict__ planes, int ncol, size_t nn,
                                                       const cplx<T>* __restrict__ v, const cplx<T>* __restrict__ z,
                                                       cplx<T>* __restrict__ grad, double* __restrict__ dotp,
                                                       const double* __restrict__ misfit, int N,
@@ -469,6 +486,14 @@ __global__ void __launch_bounds__(256) k_plane_reduce(const cplx<T>* __restrict_
         dotp[b] = s;
     }
     if (!value_out) return;   // partial launch: the value is formed by k_finalize
+    if (!v) {
+        // no shift: every <v,z> partial is 0.0, so the value needs only the
+        // misfits, final since griddepcontrol.wait -- block 0 forms it (same
+        // partition and order as the last-block path, bitwise equal) without
+        // the fence + counter round trip of every block
+        if (blockIdx.x == 0) finalize_block(misfit, N, dotp, 0, value_out, red, lin);
+        return;
+    }
     __shared__ bool last;
     if (lin == 0) {
         __threadfence();

@@ -80,6 +80,7 @@ struct Plan {
     DevMem stage_out;
 
     DevMem pos, probe;
+    DevMem probe_epi;                // complex64 TMA path: sc * P per metric (2 x M x M), sc = 1/M^2 | 2
     DevMem amp, inten;               // sqrt(d) and d, real type of the precision
     bool amp_valid = false, inten_valid = false;
 
@@ -102,6 +103,7 @@ struct Plan {
     const void* tm_amp_ptr = nullptr;
     alignas(64) unsigned char tm_probe[128] = {};
     bool tm_probe_ok = false;
+    alignas(64) unsigned char tm_probe_epi[2][128] = {};   // maps of probe_epi (one per metric)
     struct TmEntry { const void* ptr = nullptr; alignas(64) unsigned char map[128] = {}; };
     std::vector<TmEntry> tm_z_cache = std::vector<TmEntry>(8);
     size_t tm_z_next = 0;
