@@ -61,6 +61,23 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
         : "memory");
 }
 
+#ifdef ABL_TIMELINE   // diagnostic build: per-CTA globaltimer stamps (tools/timeline.py)
+__device__ unsigned long long g_tl[8192 * 8];
+__device__ __forceinline__ void tl_stamp(int k) {
+    if (threadIdx.x == 0 && blockIdx.x < 8192) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_tl[blockIdx.x * 8 + k] = t;
+        if (k == 0) g_tl[blockIdx.x * 8 + 7] = smid;
+    }
+}
+#define TL(k) tl_stamp(k)
+#else
+#define TL(k)
+#endif
+
 template <int M, int OP, bool PROBE>
 __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
     frame_tma_kernel(FrameArgs<float> a, int count, const __grid_constant__ CUtensorMap tm_z,
@@ -76,6 +93,7 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
     __shared__ __align__(8) unsigned long long bar_z[FPC], bar_a[FPC], bar_p[FPC];
     __shared__ double red[FPC * WPF];
 
+    TL(0);
     const int f = threadIdx.x / M;
     const int t = threadIdx.x % M;
     const int jl = blockIdx.x * FPC + f;
@@ -108,11 +126,18 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
     // probe column t prefetched into the (not yet live) line registers while
     // the object tile is in flight: the L2 latency hides behind the TMA
     if constexpr (PROBE) {
+#ifdef ABL_NOPREF   // ablation (timing only): no probe prefetch
+#pragma unroll
+        for (int r = 0; r < M; ++r) x[r] = make_float2(1.f + r * 1e-3f, 0.5f);
+        (void)probe;
+#else
 #pragma unroll
         for (int r = 0; r < M; ++r) x[r] = __ldg(probe + r * M + t);
+#endif
     }
     __syncthreads();
     if (live) mbar_wait(&bar_z[f], 0);
+    TL(1);
 #pragma unroll
     for (int r = 0; r < M; ++r) {   // psi = P o x, own column t
         if constexpr (PROBE) x[r] = cmul(x[r], buf[r * S + t + odd]);
@@ -125,8 +150,10 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
 #pragma unroll 1
     for (int pass = 0; pass < 4; ++pass) {
         reg_fft<M, false>(x);
+        if (pass == 1) TL(2);
         if (pass == 0) {
             // columns -> rows
+#ifndef ABL_NOTRANS
 #pragma unroll
             for (int k = 0; k < M; ++k) buf[k * S + t] = x[k];
             __syncthreads();
@@ -136,6 +163,7 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
                 x[c] = make_float2(v.x, v.y);
                 x[c + 1] = make_float2(v.z, v.w);
             }
+#endif
             __syncthreads();
             if (t == 0 && live) {   // amplitudes land while the row FFT runs
                 fence_proxy_async_smem();
@@ -165,6 +193,13 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
                         const float2 W = x[c + q];
                         const float A = Av[q];
                         float2 R;
+#ifdef ABL_NOSPEC   // ablation (timing only): trivial spectral operator
+                        if (true) {
+                            af[q] += A;
+                            x[c + q] = make_float2(W.x * A, -W.y);
+                            continue;
+                        }
+#endif
                         if constexpr (OP == OP_INTENSITY) {
                             const float r = (W.x * W.x + W.y * W.y) - A;
                             af[q] = fmaf(r, r, af[q]);
@@ -189,12 +224,14 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
         } else if (pass == 2) {
             // rows -> columns (x holds conj of the row-inverse; conjugations cancel)
             __syncthreads();   // amplitude reads done before the buffer is rewritten
+#ifndef ABL_NOTRANS
 #pragma unroll
             for (int c = 0; c < M; c += 2)
                 *reinterpret_cast<float4*>(&buf[t * S + c]) = make_float4(x[c].x, x[c].y, x[c + 1].x, x[c + 1].y);
             __syncthreads();
 #pragma unroll
             for (int r = 0; r < M; ++r) x[r] = buf[r * S + t];
+#endif
             __syncthreads();
             if constexpr (PROBE) {
                 // the buffer is idle during the last pass: TMA the probe tile in
@@ -226,6 +263,7 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
         a.misfit[j] = (OP == OP_DISTANCE) ? s / (2.0 * (double)M * (double)M) : 0.5 * s;
     }
     // let the dependent gather kernel start launching (it waits on griddepcontrol.wait)
+    TL(3);
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // epilogue: contribution = sc * conj(P) o IDFT_u(R) = conj(sc P) o conj(x)
     if (live) {
@@ -237,8 +275,12 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
 #pragma unroll
             for (int r = 0; r < M; ++r) {
                 const float2 v = PROBE ? epi_contrib_pre(x[r], buf[r * M + t]) : epi_contrib(x[r], sc);
+#ifdef ABL_NOSTORE   // ablation (timing only): no contribution stores
+                if (v.x == 1234.5f)
+#endif
                 pl[(size_t)r * a.n] = v;
             }
+            TL(4);
             return;
         }
         float2* __restrict__ out = a.stash + (size_t)j * M * S;

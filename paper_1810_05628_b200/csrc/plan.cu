@@ -1626,3 +1626,9 @@ double plan_dot(Plan& p, const void* a, const void* b, size_t len) {
 }
 
 }  // namespace ptg
+
+#ifdef ABL_TIMELINE
+extern "C" int ptg_debug_timeline(void* dst, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(dst, ptg::g_tl, bytes < sizeof(ptg::g_tl) ? bytes : sizeof(ptg::g_tl));
+}
+#endif
