@@ -307,7 +307,7 @@ void launch_cl(Plan& p, const FrameArgs<float>& a, int count, const float* data)
             h[2 * i + 1] = (float)-std::sin(th);
         }
         p.cl_tw.alloc(h.size() * sizeof(float));
-        PTG_CUDA(cudaMemcpy(p.cl_tw.p, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+        PTG_CUDA(cudaMemcpyAsync(p.cl_tw.p, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice, p.stream));
     }
     const float2* tw = p.cl_tw.as<const float2>();
     const int L = cl_line(p);
@@ -421,6 +421,15 @@ __global__ void __launch_bounds__(256, 4) k_plane_reduce(const cplx<T>* __restri
     const size_t npairs = (nn + 1) / 2;
     const size_t chunk = (npairs + kPlaneBlocks - 1) / kPlaneBlocks;
     const size_t lo = min(npairs, b * chunk), hi = min(lo + chunk, npairs);
+    if (!v && value_out && blockIdx.x == 0) {
+        // no shift: every <v,z> partial is 0.0, so the value needs only the
+        // misfits, final since griddepcontrol.wait -- block 0 forms it first
+        // (same partition and order as the last-block path, bitwise equal),
+        // overlapping the other blocks' plane reads, with no fence + counter
+        // round trip anywhere
+        finalize_block(misfit, N, dotp, 0, value_out, red, lin);
+        __syncthreads();   // red[] is reused below
+    }
     double d = 0.0;
     for (size_t pr = lo + lin / QS; pr < hi; pr += blockDim.x / QS) {
         const size_t i = 2 * pr;
@@ -486,14 +495,7 @@ __global__ void __launch_bounds__(256, 4) k_plane_reduce(const cplx<T>* __restri
         dotp[b] = s;
     }
     if (!value_out) return;   // partial launch: the value is formed by k_finalize
-    if (!v) {
-        // no shift: every <v,z> partial is 0.0, so the value needs only the
-        // misfits, final since griddepcontrol.wait -- block 0 forms it (same
-        // partition and order as the last-block path, bitwise equal) without
-        // the fence + counter round trip of every block
-        if (blockIdx.x == 0) finalize_block(misfit, N, dotp, 0, value_out, red, lin);
-        return;
-    }
+    if (!v) return;   // value formed by block 0 above
     __shared__ bool last;
     if (lin == 0) {
         __threadfence();
@@ -849,9 +851,11 @@ bool choose_planes(Plan& p) {
     p.ncolors = ncol;
     p.color_h = color;
     p.color.alloc(color.size() * sizeof(int));
-    PTG_CUDA(cudaMemcpy(p.color.p, color.data(), color.size() * sizeof(int), cudaMemcpyHostToDevice));
+    PTG_CUDA(cudaMemcpyAsync(p.color.p, color.data(), color.size() * sizeof(int), cudaMemcpyHostToDevice, p.stream));
     p.planes.alloc((size_t)ncol * p.nn() * p.celem());
-    PTG_CUDA(cudaMemset(p.planes.p, 0, p.planes.bytes));   // untouched pixels stay zero forever
+    // on the plan's (non-blocking) stream: a legacy-stream memset is not ordered
+    // before the frame kernels that store into the planes
+    PTG_CUDA(cudaMemsetAsync(p.planes.p, 0, p.planes.bytes, p.stream));   // untouched pixels stay zero forever
     return true;
 }
 
@@ -923,11 +927,11 @@ void build_chunks(Plan& p) {
         c->ntiles = (int)ids.size();
         if (!c->all_tiles) {
             c->tile_ids.alloc(ids.size() * sizeof(int));
-            if (!ids.empty()) PTG_CUDA(cudaMemcpy(c->tile_ids.p, ids.data(), ids.size() * sizeof(int), cudaMemcpyHostToDevice));
+            if (!ids.empty()) PTG_CUDA(cudaMemcpyAsync(c->tile_ids.p, ids.data(), ids.size() * sizeof(int), cudaMemcpyHostToDevice, p.stream));
         }
         // int32 stash offsets: the per-chunk stash budget keeps them < 2^31 elements
         c->tile_list.alloc(std::max<size_t>(1, list.size()) * sizeof(int4));
-        if (!list.empty()) PTG_CUDA(cudaMemcpy(c->tile_list.p, list.data(), list.size() * sizeof(int4), cudaMemcpyHostToDevice));
+        if (!list.empty()) PTG_CUDA(cudaMemcpyAsync(c->tile_list.p, list.data(), list.size() * sizeof(int4), cudaMemcpyHostToDevice, p.stream));
         p.chunks.push_back(std::move(c));
     }
     p.stash.alloc(std::max<size_t>(1, (size_t)cs * p.w * stash_pitch(p.w)) * p.celem());
@@ -994,20 +998,20 @@ std::unique_ptr<Plan> plan_create(const ptg_plan_desc& d) {
     LaunchScope ls(*p);
 
     p->pos.alloc(std::max<size_t>(1, (size_t)d.N) * sizeof(int2));
-    if (d.N) PTG_CUDA(cudaMemcpy(p->pos.p, d.positions, (size_t)d.N * sizeof(int2), cudaMemcpyHostToDevice));
+    if (d.N) PTG_CUDA(cudaMemcpyAsync(p->pos.p, d.positions, (size_t)d.N * sizeof(int2), cudaMemcpyHostToDevice, p->stream));
     if (p->has_probe) {
         p->probe_h.assign(d.probe, d.probe + 2 * p->MM());
         p->probe.alloc(p->MM() * p->celem());
         p->stage.ensure(p->MM() * 16);
-        PTG_CUDA(cudaMemcpy(p->stage.p, d.probe, p->MM() * 16, cudaMemcpyHostToDevice));
+        PTG_CUDA(cudaMemcpyAsync(p->stage.p, d.probe, p->MM() * 16, cudaMemcpyHostToDevice, p->stream));
         dev_from_c128(p->prec, p->probe.p, p->stage.as<double>(), p->MM(), p->stream);
     }
     build_chunks(*p);
     p->value.alloc(4 * sizeof(double));
     p->counter.alloc(sizeof(unsigned int) * 4);
-    PTG_CUDA(cudaMemset(p->counter.p, 0, p->counter.bytes));
+    PTG_CUDA(cudaMemsetAsync(p->counter.p, 0, p->counter.bytes, p->stream));
     p->scratch.alloc((kReduceBlocks + 2) * sizeof(double));
-    PTG_CUDA(cudaMemset(p->scratch.p, 0, p->scratch.bytes));
+    PTG_CUDA(cudaMemsetAsync(p->scratch.p, 0, p->scratch.bytes, p->stream));
     p->flag.alloc(sizeof(unsigned long long));
     p->hval.ensure(4 * sizeof(double));
     if (d.data) plan_set_data_host(*p, d.data, d.data_dtype);
