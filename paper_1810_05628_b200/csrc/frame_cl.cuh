@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
     float2* tw = buf + L * PM;                           // W_M^i, i < M
     __shared__ double red[NT / 32];
 
+    TL(0);
     const int q = (int)cl.block_rank();
     const int j = a.first + (int)(blockIdx.x / Q);
     const int t = threadIdx.x;
@@ -137,6 +138,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         }
     }
     cl.sync();
+    TL(1);
 
     // row-stage roles: butterflies (row g + Q i, element m); FFT64 quarter-rows (rr, qq)
     const int m = t % L, g = t / L;
@@ -213,6 +215,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                 }
             }
             acc = ((double)af[0] + (double)af[1]) + ((double)af[2] + (double)af[3]);
+            TL(2);
         } else if (pass == 2) {
 #pragma unroll
             for (int c = 0; c < L; c += 2)
@@ -252,7 +255,9 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((t & 31) == 0) red[t / 32] = acc;
+    TL(3);
     cl.sync();   // every push has landed; no remote access after this point
+    TL(4);
     if (t == 0) {
         double s = 0.0;
 #pragma unroll
@@ -292,6 +297,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
             }
         }
     }
+    TL(5);
 }
 
 // [j][q][r][p][k] = A_j[Q r + q][Q k + p]: amplitudes in the order the cluster

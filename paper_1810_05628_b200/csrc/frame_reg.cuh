@@ -28,6 +28,23 @@
 
 namespace ptg {
 
+#ifdef ABL_TIMELINE   // diagnostic build: per-CTA globaltimer stamps (tools/timeline.py)
+__device__ unsigned long long g_tl[8192 * 8];
+__device__ __forceinline__ void tl_stamp(int k) {
+    if (threadIdx.x == 0 && blockIdx.x < 8192) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_tl[blockIdx.x * 8 + k] = t;
+        if (k == 0) g_tl[blockIdx.x * 8 + 7] = smid;
+    }
+}
+#define TL(k) tl_stamp(k)
+#else
+#define TL(k)
+#endif
+
 // ------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);

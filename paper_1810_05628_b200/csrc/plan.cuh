@@ -78,6 +78,14 @@ struct Plan {
     cudaStream_t s_in = nullptr, s_out = nullptr;
     std::vector<cudaEvent_t> ev_band;
     DevMem stage_out;
+    // the banded host evaluation replayed as one CUDA graph (pinned host
+    // buffers): keyed on every pointer the captured sequence bakes in; the
+    // first call with a key runs eagerly, the second captures
+    struct HostGraph {
+        cudaGraphExec_t exec = nullptr;
+        std::vector<const void*> key, seen;
+        int64_t launches = 0;   // kernels per replay (launch accounting)
+    } hg;
 
     DevMem pos, probe;
     DevMem probe_epi;                // complex64 TMA path: sc * P per metric (2 x M x M), sc = 1/M^2 | 2

@@ -268,3 +268,39 @@ def test_banded_host_eval_equals_device_eval(cfg_id, with_shift):
     val_d = plan.evaluate_device(zt, gt, v=vt)
     assert val_h == val_d
     assert np.array_equal(g_h, gt.cpu().numpy().astype(np.complex128))
+
+
+@pytest.mark.parametrize("with_shift", [False, True])
+def test_graph_replayed_host_eval(with_shift):
+    """With pinned host buffers ptg_eval replays the banded sequence as one CUDA
+    graph (first call eager, second captured, later calls replayed).  Every call
+    sees the current contents of z / v and equals the device evaluation bitwise;
+    new buffers (another key) fall back to eager and are captured again."""
+    import torch
+    from paper_1810_05628_b200 import Plan, synth
+    cfg = synth.CONFIGS[2]
+    obj, probe, pos = synth.make_inputs(cfg)
+    plan = Plan(cfg.n, cfg.M, cfg.w, pos, None, probe, precision="c64")
+    plan.simulate(obj, copy_out=False)
+    n = cfg.n
+    zp = torch.empty(n, n, dtype=torch.complex128).pin_memory()
+    gp = torch.empty(n, n, dtype=torch.complex128).pin_memory()
+    vp = torch.empty(n, n, dtype=torch.complex128).pin_memory() if with_shift else None
+    for call in range(5):
+        if call == 3:   # new pointers: eager again, then re-captured
+            zp = torch.empty(n, n, dtype=torch.complex128).pin_memory()
+            gp = torch.empty(n, n, dtype=torch.complex128).pin_memory()
+        z = (obj * (0.9 - 0.05 * call) + 0.05 * rand_field(n, 20 + call)).astype(np.complex64).astype(np.complex128)
+        zp.numpy()[:] = z
+        v = None
+        if with_shift:
+            v = (0.01 * rand_field(n, 40 + call)).astype(np.complex64).astype(np.complex128)
+            vp.numpy()[:] = v
+        gp.numpy()[:] = np.nan
+        val_h, _ = plan.evaluate(zp.numpy(), None if vp is None else vp.numpy(), out=gp.numpy())
+        zt = torch.from_numpy(z.astype(np.complex64)).cuda()
+        vt = torch.from_numpy(v.astype(np.complex64)).cuda() if v is not None else None
+        gt = torch.empty_like(zt)
+        val_d = plan.evaluate_device(zt, gt, v=vt)
+        assert val_h == val_d, call
+        assert np.array_equal(gp.numpy(), gt.cpu().numpy().astype(np.complex128)), call

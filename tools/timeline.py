@@ -34,19 +34,25 @@ torch.cuda.synchronize()
 lib = _lib.lib()
 buf = np.zeros(8192 * 8, dtype=np.uint64)
 lib.ptg_debug_timeline(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes))
-nb = cfg.N
+if cfg.M <= 64:
+    nb, K = cfg.N, 5
+    names = ["start", "obj landed", "rows FFT done", "passes done", "stored"]
+else:
+    nb, K = min(8192, cfg.N * (cfg.M // 32)), 6
+    names = ["start", "gather+sync", "spectral done", "pushes done", "cluster sync", "stored"]
 t = buf.reshape(8192, 8)[:nb].astype(np.int64)
 t0 = t[:, 0].min()
-rel = (t[:, :5] - t0) / 1e3
-names = ["start", "obj landed", "rows FFT done", "passes done", "stored"]
-for k in range(5):
+rel = (t[:, :K] - t0) / 1e3
+for k in range(K):
     print(f"{names[k]:14s} min {rel[:, k].min():7.2f}  p50 {np.median(rel[:, k]):7.2f}  max {rel[:, k].max():7.2f} us")
-for k in range(1, 5):
+for k in range(1, K):
     d = rel[:, k] - rel[:, k - 1]
     print(f"phase {names[k-1]:>14s} -> {names[k]:14s}: p10 {np.percentile(d, 10):6.2f} p50 {np.median(d):6.2f} p90 {np.percentile(d, 90):6.2f} us")
 sm = t[:, 7]
 last = {}
 for i in range(nb):
-    last[sm[i]] = max(last.get(sm[i], 0), rel[i, 4])
+    last[sm[i]] = max(last.get(sm[i], 0), rel[i, K - 1])
 v = np.array(list(last.values()))
+life = rel[:, K - 1] - rel[:, 0]
+print(f"CTA lifetime p10 {np.percentile(life, 10):.2f} p50 {np.median(life):.2f} p90 {np.percentile(life, 90):.2f} us")
 print(f"per-SM finish: min {v.min():.2f} p50 {np.median(v):.2f} max {v.max():.2f} us over {len(v)} SMs")
