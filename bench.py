@@ -341,6 +341,8 @@ def run_ours(args):
     achieved_gbs = B / avg_frame_s / 1e9
     sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
     fp32_peak = N_SM * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+    if cfg.precision == "c128":   # complex128 frames compute in FP64: 64 FP64 lanes per SM on B200
+        fp32_peak /= 2
     achieved_tf = F / avg_frame_s / 1e12
     traffic = load_traffic(f"config{cfg.cid}_frame_kernel")
     kname = (f"frame_tma_kernel<{cfg.M}> (TMA-fed register FFT, one CTA per scan position)" if cfg.M <= 64 and cfg.precision == "c64"
@@ -350,10 +352,13 @@ def run_ours(args):
                     "frac": achieved_gbs / hbm_peak, "traffic": traffic,
                     "algorithmic_bytes_per_launch": B / launches_per_eval,
                     "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)"}
-    roofline_fp32 = {"bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
+    roofline_fp32 = {"bound": "fp32" if cfg.precision == "c64" else "fp64", "achieved": achieved_tf, "peak": fp32_peak,
+                     "unit": "TFLOP/s",
                      "frac": achieved_tf / fp32_peak, "algorithmic_flops_per_launch": F / launches_per_eval,
                      "convention": "F(M)=10 M^2 log2(M^2) + 24 M^2 per pattern (SURVEY 8d)",
-                     "peak_source": f"nominal 148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (no measured FP32 figure)"}
+                     "peak_source": (f"nominal 148 SM x 128 FP32 lanes x 2 x {sm_mhz:.0f} MHz (no measured FP32 figure; "
+                                     "tools/fp32_tput.cu measures 116-124 lane-ops/SM/clk for FFMA/FFMA2/FADD2)")
+                     if cfg.precision == "c64" else f"nominal 148 SM x 64 FP64 lanes x 2 x {sm_mhz:.0f} MHz"}
     # the headline roofline is the binding one of SURVEY 8(d): attainable time
     # = max(B / BW_HBM, F / P_FP32); the frame kernel is FP32-bound at every
     # configuration (no tensor cores on this path), the HBM view is kept beside it
@@ -431,7 +436,7 @@ def run_ours(args):
             torch.cuda.synchronize()
             cyc = []
             per = None
-            for _ in range(3):
+            for _ in range(7):   # wall-clock (one host sync per coarse LBFGS iteration): median of 7
                 t0 = time.perf_counter()
                 v3, wt, per = h3.cycle_device(z3, g3, v3)
                 torch.cuda.synchronize()
