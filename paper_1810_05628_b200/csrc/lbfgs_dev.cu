@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <new>
 
 #include "solvers.cuh"
 
@@ -347,9 +348,23 @@ __global__ void __launch_bounds__(kReduceThreads) k_pair_stats(const cplx<T>* nz
     __syncthreads();
     if (!last) return;
     __threadfence();
+    // all five quantities' partials in flight together (one L2 round trip), then
+    // the same per-thread order and trees as a loop per quantity (same bits)
+    constexpr int PER = (kPsBlocks + kReduceThreads - 1) / kReduceThreads;
+    double v[5][PER];
+#pragma unroll
+    for (int q = 0; q < 5; ++q)
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int i = threadIdx.x + u * kReduceThreads;
+            v[q][u] = i < kPsBlocks ? __ldcg(scratch + q * kReduceBlocks + i) : 0.0;
+        }
+#pragma unroll
     for (int q = 0; q < 5; ++q) {
         double t = 0.0;
-        for (int i = threadIdx.x; i < kPsBlocks; i += kReduceThreads) t += __ldcg(scratch + q * kReduceBlocks + i);
+#pragma unroll
+        for (int u = 0; u < PER; ++u)
+            if (threadIdx.x + u * kReduceThreads < kPsBlocks) t += v[q][u];
         t = warp_tree(t);
         __syncthreads();
         if (lane == 0) red[0][w] = t;
@@ -445,6 +460,9 @@ struct CombineArgs {
     const cplx<T>* g;
     cplx<T>* dir;
     size_t len;
+    // optional fused first line-search trial: trial = z0 + 1 * dir (k_add_scaled's arithmetic)
+    const cplx<T>* z0;
+    cplx<T>* trial;
 };
 
 template <typename T>
@@ -469,7 +487,13 @@ __global__ void __launch_bounds__(256) k_combine(const CombineArgs<T> a) {
                     ry = fma(a.u[j], (double)sv[q].y, fma(a.c[j], (double)yv[q].y, ry));
                 }
         }
-        a.dir[i] = mk<T>((T)-rx, (T)-ry);
+        const cplx<T> d = mk<T>((T)-rx, (T)-ry);
+        a.dir[i] = d;
+        if (a.trial) {
+            const T one = (T)1.0;
+            const cplx<T> u = a.z0[i];
+            a.trial[i] = mk<T>(u.x + one * d.x, u.y + one * d.y);
+        }
     }
 }
 
@@ -600,6 +624,112 @@ void dev_pair_stats(const Plan& p, const void* nz, const void* z, const void* ng
             (const double2*)nz, (const double2*)z, (const double2*)ng, (const double2*)g, (double2*)s_out,
             (double2*)y_out, len, scratch, out_dev);
     PTG_CHECK_LAUNCH();
+    count_launch();
+}
+
+// ------------------------------------------ kernel-node parameters (graphs)
+// The same launches as dev_combine / dev_pair_stats / dev_multi_dot, as
+// cudaKernelNodeParams: d_lbfgs replays its per-iteration sequence as a CUDA
+// graph and rewrites these nodes' arguments each iteration.
+namespace {
+template <typename A>
+A& node_store(KNode& n) {
+    static_assert(sizeof(A) <= sizeof(n.store), "KNode store too small");
+    return *new (n.store) A();
+}
+template <typename T>
+void node_combine_t(const Plan& p, const void* const* s, const void* const* y, const double* u, const double* c,
+                    double gamma, int k, const void* g, void* dir, KNode& n, const void* z0, void* trial) {
+    CombineArgs<T>& a = node_store<CombineArgs<T>>(n);
+    for (int i = 0; i < k; ++i) {
+        a.s[i] = static_cast<const cplx<T>*>(s[i]);
+        a.y[i] = static_cast<const cplx<T>*>(y[i]);
+        a.u[i] = u[i];
+        a.c[i] = c[i];
+    }
+    a.gamma = gamma;
+    a.k = k;
+    a.g = static_cast<const cplx<T>*>(g);
+    a.dir = static_cast<cplx<T>*>(dir);
+    a.len = p.nn();
+    a.z0 = static_cast<const cplx<T>*>(z0);
+    a.trial = static_cast<cplx<T>*>(trial);
+    n.argp[0] = &a;
+    n.prm = cudaKernelNodeParams{};
+    n.prm.func = reinterpret_cast<void*>(k_combine<T>);
+    n.prm.gridDim = dim3((unsigned)std::min<size_t>(148 * 8, (a.len + 255) / 256));
+    n.prm.blockDim = dim3(256);
+    n.prm.kernelParams = n.argp;
+}
+struct PairStatsArgs {
+    const void *nz, *z, *ng, *g;
+    void *s, *y;
+    size_t len;
+    double *scratch, *out;
+};
+template <typename T>
+void node_multi_dot_t(const Plan& p, const void* const* s, const void* const* y, int A, const void* yc,
+                      const void* gn, double* scratch, double* out_dev, KNode& md, KNode& ms) {
+    MultiDotArgs<T>& a = node_store<MultiDotArgs<T>>(md);
+    for (int i = 0; i < A; ++i) {
+        a.s[i] = static_cast<const cplx<T>*>(s[i]);
+        a.y[i] = static_cast<const cplx<T>*>(y[i]);
+    }
+    a.yc = static_cast<const cplx<T>*>(yc);
+    a.gn = static_cast<const cplx<T>*>(gn);
+    a.A = A;
+    a.len = p.nn();
+    a.partial = scratch;
+    md.argp[0] = &a;
+    md.prm = cudaKernelNodeParams{};
+    md.prm.func = reinterpret_cast<void*>(k_multi_dot<T>);
+    md.prm.gridDim = dim3(kMdBlocks, (A + kMdPairs - 1) / kMdPairs);
+    md.prm.blockDim = dim3(kReduceThreads);
+    md.prm.kernelParams = md.argp;
+    struct MS { const double* partial; double* out; };
+    MS& b = node_store<MS>(ms);
+    b.partial = scratch;
+    b.out = out_dev;
+    ms.argp[0] = &b.partial;
+    ms.argp[1] = &b.out;
+    ms.prm = cudaKernelNodeParams{};
+    ms.prm.func = reinterpret_cast<void*>(k_multi_sum);
+    ms.prm.gridDim = dim3(4 * A);
+    ms.prm.blockDim = dim3(kReduceThreads);
+    ms.prm.kernelParams = ms.argp;
+}
+}  // namespace
+
+void node_combine(const Plan& p, const void* const* s, const void* const* y, const double* u, const double* c,
+                  double gamma, int k, const void* g, void* dir, KNode& n, const void* z0, void* trial) {
+    if (k > kMaxPairs) raise(PTG_ERR_INTERNAL, "combine: too many pairs");
+    if (p.prec == PTG_C64) node_combine_t<float>(p, s, y, u, c, gamma, k, g, dir, n, z0, trial);
+    else node_combine_t<double>(p, s, y, u, c, gamma, k, g, dir, n, z0, trial);
+}
+
+void node_pair_stats(const Plan& p, const void* nz, const void* z, const void* ng, const void* g, void* s_out,
+                     void* y_out, double* scratch, double* out_dev, KNode& n) {
+    PairStatsArgs& a = node_store<PairStatsArgs>(n);
+    a = PairStatsArgs{nz, z, ng, g, s_out, y_out, p.nn(), scratch, out_dev};
+    void* ptrs[9] = {&a.nz, &a.z, &a.ng, &a.g, &a.s, &a.y, &a.len, &a.scratch, &a.out};
+    for (int i = 0; i < 9; ++i) n.argp[i] = ptrs[i];
+    n.prm = cudaKernelNodeParams{};
+    n.prm.func = p.prec == PTG_C64 ? reinterpret_cast<void*>(k_pair_stats<float>)
+                                   : reinterpret_cast<void*>(k_pair_stats<double>);
+    n.prm.gridDim = dim3(kPsBlocks);
+    n.prm.blockDim = dim3(kReduceThreads);
+    n.prm.kernelParams = n.argp;
+}
+
+void node_multi_dot(const Plan& p, const void* const* s, const void* const* y, int A, const void* yc,
+                    const void* gn, double* scratch, double* out_dev, KNode& md, KNode& ms) {
+    if (A <= 0 || A > kMaxPairs + 1) raise(PTG_ERR_INTERNAL, "multi_dot: pair count");
+    if (p.prec == PTG_C64) node_multi_dot_t<float>(p, s, y, A, yc, gn, scratch, out_dev, md, ms);
+    else node_multi_dot_t<double>(p, s, y, A, yc, gn, scratch, out_dev, md, ms);
+}
+
+void node_launch(const KNode& n, cudaStream_t s) {
+    PTG_CUDA(cudaLaunchKernel(n.prm.func, n.prm.gridDim, n.prm.blockDim, n.prm.kernelParams, n.prm.sharedMemBytes, s));
     count_launch();
 }
 

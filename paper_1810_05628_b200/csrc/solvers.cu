@@ -1,5 +1,6 @@
 // solvers.cu — GPU-resident line search / LBFGS / MG/OPT (see solvers.cuh).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <string>
@@ -8,6 +9,14 @@
 #include "transfer.cuh"
 
 namespace ptg {
+
+// PTG_LBFGS_DEBUG=1: host time inside the line-search synchronisations vs the
+// whole LBFGS call (dev instrumentation)
+static double g_sync_us = 0.0;
+static bool lbfgs_debug() {
+    static const bool on = getenv("PTG_LBFGS_DEBUG") != nullptr;
+    return on;
+}
 
 void DObj::eval_enqueue(Counter& c, const void* z, void* grad, double* host_value) const {
     Plan& p = *plan;
@@ -39,6 +48,42 @@ LsOut d_linesearch(const DObj& obj, const void* z, const void* dir, Counter& ctr
         dev_add_scaled(p.prec, z_out, z, alpha, dir, len, p.stream);   // z + alpha d
         obj.eval_enqueue(ctr, z_out, g_out, h);
         if (t == 0 && first_trial_hook) first_trial_hook();
+        const auto ts = std::chrono::steady_clock::now();
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+        if (lbfgs_debug()) g_sync_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ts).count();
+        const double v = h[0];
+        ++r.trials;
+        if (v <= base) {
+            r.alpha = alpha;
+            r.value = v;
+            return r;
+        }
+        alpha *= 0.5;
+    }
+    r.alpha = 0.0;
+    r.stalled = true;
+    dev_copy(p.prec, z_out, z, len, p.stream);
+    return r;
+}
+
+// the rest of d_linesearch after its first trial (alpha = 1, value v1) ran
+// elsewhere (the graph-replayed LBFGS iteration): same trials, same charges
+LsOut d_linesearch_continue(const DObj& obj, const void* z, const void* dir, Counter& ctr, int max_trials,
+                            double base, void* z_out, void* g_out, double v1) {
+    Plan& p = *obj.plan;
+    const size_t len = p.nn();
+    double* h = p.hval.as<double>();
+    LsOut r;
+    r.trials = 1;
+    if (v1 <= base) {
+        r.alpha = 1.0;
+        r.value = v1;
+        return r;
+    }
+    double alpha = 0.5;
+    for (int t = 1; t < max_trials; ++t) {
+        dev_add_scaled(p.prec, z_out, z, alpha, dir, len, p.stream);
+        obj.eval_enqueue(ctr, z_out, g_out, h);
         PTG_CUDA(cudaStreamSynchronize(p.stream));
         const double v = h[0];
         ++r.trials;
@@ -91,6 +136,9 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                  std::vector<ptg_hist>* hist) {
     Plan& p = *obj.plan;
     LaunchScope ls(p);
+    const auto t_call = std::chrono::steady_clock::now();
+    g_sync_us = 0.0;
+    int iters_done = 0;
     const size_t len = p.nn();
     DVec z(p, len), g(p, len), dir(p, len), nz(p, len), ng(p, len);
     dev_copy(p.prec, z.p, z0, len, p.stream);
@@ -118,7 +166,13 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     DVec ws;   // fused-kernel scratch (two-loop partials / pair statistics / products)
     double* wsd = nullptr;
     p.hval.ensure(8 * sizeof(double));
-    double* stats_h = p.hval.as<double>() + 2;   // [0] = line-search value
+    // pinned results of an iteration: [0] first trial's value, [1..5] pair
+    // statistics, [9..] compact-mode products -- one block so the graph-replayed
+    // iteration reads them back with a single copy
+    constexpr size_t kRes = 9 + 4 * (size_t)(kMaxPairs + 1);
+    HostPinned res_h;
+    res_h.ensure(kRes * sizeof(double));
+    double* stats_h = res_h.as<double>() + 1;
     // Direction: "compact" (default) — the compact representation of the same
     // LBFGS matrix (Byrd, Nocedal & Schnabel 1994): the O(k) products it needs
     // are batched into one pass per iteration and ride on the line search's
@@ -137,20 +191,32 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
         Sg.assign(nslot_max, 0.0);
         Yg.assign(nslot_max, 0.0);
     }
-    HostPinned md_h;
     double gg = g0 * g0;   // <g, g> of the current gradient
+    // per-iterate-buffer graphs of the compact iteration (PTG_LBFGS_GRAPH=0: eager)
+    struct IterGraph {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        cudaGraphNode_t nc = nullptr, nps = nullptr, nmd = nullptr, nms = nullptr;
+        const void* z = nullptr;
+        int64_t launches = 0;
+        ~IterGraph() {
+            if (exec) cudaGraphExecDestroy(exec);
+            if (graph) cudaGraphDestroy(graph);
+        }
+    } ig[2];
+    static const bool use_graph = !(getenv("PTG_LBFGS_GRAPH") && getenv("PTG_LBFGS_GRAPH")[0] == '0');
     if (satisfied(gnorm)) {
         out.reason = PTG_STOP_TOLERANCE;
     } else {
         ws.s = p.stream;
-        ws.bytes = ((size_t)kPairScratch + 8 + (compact ? kMultiDotScratch + 4 * (kMaxPairs + 1) : 0)) * sizeof(double);
+        ws.bytes = ((size_t)kPairScratch + kMultiDotScratch + kRes) * sizeof(double);
         PTG_CUDA(cudaMallocAsync(&ws.p, ws.bytes, p.stream));
         PTG_CUDA(cudaMemsetAsync(ws.p, 0, ws.bytes, p.stream));
         wsd = static_cast<double*>(ws.p);
-        double* stats_d = wsd + kPairScratch;
-        double* md_scratch = stats_d + 8;
-        double* md_d = md_scratch + kMultiDotScratch;
-        if (compact) md_h.ensure(4 * (kMaxPairs + 1) * sizeof(double));
+        double* md_scratch = wsd + kPairScratch;
+        double* res_d = md_scratch + kMultiDotScratch;   // device image of res_h
+        double* stats_d = res_d + 1;
+        double* md_d = res_d + 9;
         for (int iter = 1; iter <= cfg.max_iters; ++iter) {
             std::vector<const void*> sp, yp;
             std::vector<double> syv;
@@ -160,9 +226,16 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                 syv.push_back(slots[id].sy);
             }
             const int k = (int)order.size();
+            const bool graph_iter = compact && use_graph && iter > 2 && cfg.linesearch_max >= 1 && !p.timing;
+            // compact mode: the direction launch is a kernel node (k_combine;
+            // gamma = 1, no pairs = steepest descent, bitwise -g); replayed
+            // iterations also form the first trial nz = z + dir in it
+            const void* tz = graph_iter ? z.p : nullptr;
+            void* tn = graph_iter ? nz.p : nullptr;
+            KNode nc, nps, nmd, nms;
             if (compact) {
                 if (k == 0) {
-                    dev_scale(p.prec, dir.p, g.p, -1.0, len, p.stream);
+                    node_combine(p, nullptr, nullptr, nullptr, nullptr, 1.0, 0, g.p, dir.p, nc, tz, tn);
                 } else {
                     // H g = gamma g + [S, gamma Y] [[R^-T (D + gamma Y'Y) R^-1, -R^-T], [-R^-1, 0]] [S'g; gamma Y'g]
                     auto sy = [&](int i, int j) { return SY[(size_t)order[i] * nslot_max + order[j]]; };
@@ -189,8 +262,8 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                         c[i] = -gamma * t[i];
                         dg += u[i] * Sg[order[i]] + c[i] * Yg[order[i]];
                     }
-                    if (-dg >= 0.0) dev_scale(p.prec, dir.p, g.p, -1.0, len, p.stream);   // descent check
-                    else dev_combine(p, sp.data(), yp.data(), u.data(), c.data(), gamma, k, g.p, dir.p);
+                    if (-dg >= 0.0) node_combine(p, nullptr, nullptr, nullptr, nullptr, 1.0, 0, g.p, dir.p, nc, tz, tn);   // descent check
+                    else node_combine(p, sp.data(), yp.data(), u.data(), c.data(), gamma, k, g.p, dir.p, nc, tz, tn);
                 }
             } else {
                 // fused two-loop + descent check, else the kernel-per-op path
@@ -215,16 +288,89 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
             std::vector<const void*> msp(sp), myp(yp);
             msp.push_back(pr.s.p);
             myp.push_back(pr.y.p);
+            if (compact) {
+                node_pair_stats(p, nz.p, z.p, ng.p, g.p, pr.s.p, pr.y.p, wsd, stats_d, nps);
+                node_multi_dot(p, msp.data(), myp.data(), k + 1, pr.y.p, ng.p, md_scratch, md_d, nmd, nms);
+            }
             auto stats = [&]() {
-                dev_pair_stats(p, nz.p, z.p, ng.p, g.p, pr.s.p, pr.y.p, wsd, stats_d);
-                PTG_CUDA(cudaMemcpyAsync(stats_h, stats_d, 5 * sizeof(double), cudaMemcpyDeviceToHost, p.stream));
                 if (compact) {
-                    dev_multi_dot(p, msp.data(), myp.data(), k + 1, pr.y.p, ng.p, md_scratch, md_d);
-                    PTG_CUDA(cudaMemcpyAsync(md_h.p, md_d, 4 * (size_t)(k + 1) * sizeof(double),
+                    node_launch(nps, p.stream);
+                    PTG_CUDA(cudaMemcpyAsync(stats_h, stats_d, 5 * sizeof(double), cudaMemcpyDeviceToHost, p.stream));
+                    node_launch(nmd, p.stream);
+                    node_launch(nms, p.stream);
+                    // fixed size (graph replay: the memcpy node is not rewritten)
+                    PTG_CUDA(cudaMemcpyAsync(res_h.as<double>() + 9, md_d, 4 * (size_t)(kMaxPairs + 1) * sizeof(double),
                                              cudaMemcpyDeviceToHost, p.stream));
+                } else {
+                    dev_pair_stats(p, nz.p, z.p, ng.p, g.p, pr.s.p, pr.y.p, wsd, stats_d);
+                    PTG_CUDA(cudaMemcpyAsync(stats_h, stats_d, 5 * sizeof(double), cudaMemcpyDeviceToHost, p.stream));
                 }
             };
-            LsOut lsr = d_linesearch(obj, z.p, dir.p, ctr, cfg.linesearch_max, &cur, nz.p, ng.p, stats);
+            LsOut lsr;
+            if (graph_iter) {
+                // direction + first trial (alpha = 1) + its evaluation + the pair
+                // statistics and products, as one graph launch per iterate
+                // buffer (z / nz swap): ~10 launches' host cost -> one launch and
+                // four node-argument updates
+                IterGraph& G = ig[0].z == z.p ? ig[0] : ig[1].z == z.p ? ig[1] : ig[0].exec ? ig[1] : ig[0];
+                if (!G.exec) {
+                    const int64_t l0 = p.launches;
+                    PTG_CUDA(cudaStreamBeginCapture(p.stream, cudaStreamCaptureModeThreadLocal));
+                    cudaGraph_t gr = nullptr;
+                    try {
+                        node_launch(nc, p.stream);                              // dir and nz = z + dir
+                        ctr.record(obj.level, obj.weight);                      // charge before evaluating
+                        plan_eval(p, obj.metric, nz.p, obj.v, ng.p, res_d);     // value -> res_d[0]
+                        node_launch(nps, p.stream);                             // -> res_d[1..5]
+                        node_launch(nmd, p.stream);
+                        node_launch(nms, p.stream);                             // -> res_d[9..]
+                        PTG_CUDA(cudaMemcpyAsync(res_h.p, res_d, kRes * sizeof(double), cudaMemcpyDeviceToHost,
+                                                 p.stream));
+                    } catch (...) {
+                        cudaStreamEndCapture(p.stream, &gr);
+                        if (gr) cudaGraphDestroy(gr);
+                        throw;
+                    }
+                    PTG_CUDA(cudaStreamEndCapture(p.stream, &gr));
+                    G.graph = gr;
+                    PTG_CUDA(cudaGraphInstantiate(&G.exec, gr, 0));
+                    G.launches = p.launches - l0;
+                    size_t nn_ = 0;
+                    PTG_CUDA(cudaGraphGetNodes(gr, nullptr, &nn_));
+                    std::vector<cudaGraphNode_t> nodes(nn_);
+                    PTG_CUDA(cudaGraphGetNodes(gr, nodes.data(), &nn_));
+                    for (auto nd : nodes) {
+                        cudaGraphNodeType ty;
+                        PTG_CUDA(cudaGraphNodeGetType(nd, &ty));
+                        if (ty != cudaGraphNodeTypeKernel) continue;
+                        cudaKernelNodeParams kp{};
+                        PTG_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+                        if (kp.func == nc.prm.func) G.nc = nd;
+                        else if (kp.func == nps.prm.func) G.nps = nd;
+                        else if (kp.func == nmd.prm.func) G.nmd = nd;
+                        else if (kp.func == nms.prm.func) G.nms = nd;
+                    }
+                    if (!G.nc || !G.nps || !G.nmd || !G.nms) raise(PTG_ERR_INTERNAL, "lbfgs graph: node lookup");
+                    G.z = z.p;
+                } else {
+                    PTG_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, G.nc, &nc.prm));
+                    PTG_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, G.nps, &nps.prm));
+                    PTG_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, G.nmd, &nmd.prm));
+                    PTG_CUDA(cudaGraphExecKernelNodeSetParams(G.exec, G.nms, &nms.prm));
+                    ctr.record(obj.level, obj.weight);   // charge before evaluating (solvers.hpp:33-36)
+                    p.launches += G.launches;
+                }
+                PTG_CUDA(cudaGraphLaunch(G.exec, p.stream));
+                const auto ts = std::chrono::steady_clock::now();
+                PTG_CUDA(cudaStreamSynchronize(p.stream));
+                if (lbfgs_debug())
+                    g_sync_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ts).count();
+                lsr = d_linesearch_continue(obj, z.p, dir.p, ctr, cfg.linesearch_max, cur, nz.p, ng.p,
+                                            res_h.as<double>()[0]);
+            } else {
+                if (compact) node_launch(nc, p.stream);
+                lsr = d_linesearch(obj, z.p, dir.p, ctr, cfg.linesearch_max, &cur, nz.p, ng.p, stats);
+            }
             if (lsr.stalled) {
                 out.reason = PTG_STOP_STALL;
                 break;
@@ -237,7 +383,7 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
             pr.sy = stats_h[0];
             const bool accept = pr.sy > 1e-12 * std::sqrt(stats_h[1]) * std::sqrt(stats_h[2]);
             if (compact) {
-                const double* md = md_h.as<double>();
+                const double* md = res_h.as<double>() + 9;
                 for (int a = 0; a <= k; ++a) {
                     const int sa = a < k ? order[a] : slot;
                     if (accept) {
@@ -256,6 +402,7 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
             }
             std::swap(z, nz);
             std::swap(g, ng);
+            ++iters_done;
             cur = lsr.value;
             gnorm = std::sqrt(stats_h[3]);
             if (hist) hist->push_back({ctr.weighted, cur, gnorm});
@@ -273,6 +420,11 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     if (g_out) dev_copy(p.prec, g_out, g.p, len, p.stream);
     out.value = cur;
     PTG_CUDA(cudaStreamSynchronize(p.stream));
+    if (lbfgs_debug() && iters_done > 0) {
+        const double tot = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_call).count();
+        fprintf(stderr, "[lbfgs] n=%d iters %d: %.1f us/iter wall, %.1f us/iter in line-search syncs\n", p.n,
+                iters_done, tot / iters_done, g_sync_us / iters_done);
+    }
     return out;
 }
 

@@ -119,6 +119,24 @@ constexpr int kPairScratch = 5 * kReduceBlocks + 2;
 void dev_pair_stats(const Plan& p, const void* nz, const void* z, const void* ng, const void* g, void* s_out,
                     void* y_out, double* scratch, double* out_dev);
 
+// The launches of dev_combine / dev_pair_stats / dev_multi_dot (+ its sum)
+// as kernel-node parameters with their argument storage, for graph replay
+// (d_lbfgs rewrites them in an instantiated graph every iteration).
+struct KNode {
+    cudaKernelNodeParams prm{};
+    void* argp[12] = {};
+    alignas(16) unsigned char store[2 * (kMaxPairs + 1) * 8 + 2 * kMaxPairs * 8 + 128] = {};
+};
+// z0 / trial (optional): also form the first line-search trial z0 + 1 * dir
+void node_combine(const Plan& p, const void* const* s, const void* const* y, const double* u, const double* c,
+                  double gamma, int k, const void* g, void* dir, KNode& n, const void* z0 = nullptr,
+                  void* trial = nullptr);
+void node_pair_stats(const Plan& p, const void* nz, const void* z, const void* ng, const void* g, void* s_out,
+                     void* y_out, double* scratch, double* out_dev, KNode& n);
+void node_multi_dot(const Plan& p, const void* const* s, const void* const* y, int A, const void* yc,
+                    const void* gn, double* scratch, double* out_dev, KNode& md, KNode& ms);
+void node_launch(const KNode& n, cudaStream_t s);
+
 // solvers.cpp:87-141.  warm_g (device) with *warm_value, or null to evaluate.
 SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Counter& ctr,
                  const double* warm_value, const void* warm_g, void* z_out, void* g_out,
