@@ -966,6 +966,24 @@ void check_device(int device) {
 }  // namespace
 
 // ------------------------------------------------------------------ create
+// The solvers' work vectors are stream-ordered allocations (cudaMallocAsync).
+// With the default pool release threshold (0) every synchronisation hands the
+// freed memory back to the driver and the next allocation maps it again
+// (~100 us for a few MB): an MG/OPT cycle allocates ~30 vectors per level.
+// Keep the pool's memory reserved instead (bounded by the peak working set).
+static void keep_pool_memory(int device) {
+    static bool done[64] = {};
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    uint64_t thr = ~0ull;
+    PTG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    done[device] = true;
+}
+
 std::unique_ptr<Plan> plan_create(const ptg_plan_desc& d) {
     if (d.n < 1) raise(PTG_ERR_GEOMETRY, "object side must be positive");
     if (!is_pow2(d.M))
@@ -997,6 +1015,7 @@ std::unique_ptr<Plan> plan_create(const ptg_plan_desc& d) {
     p->pos_h.assign(d.positions, d.positions + 2 * (size_t)d.N);
     PTG_CUDA(cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking));
     p->stream = p->own_stream;
+    keep_pool_memory(p->device);
     LaunchScope ls(*p);
 
     p->pos.alloc(std::max<size_t>(1, (size_t)d.N) * sizeof(int2));

@@ -137,6 +137,13 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     Plan& p = *obj.plan;
     LaunchScope ls(p);
     const auto t_call = std::chrono::steady_clock::now();
+    std::string dbg_log;
+    auto dbg_mark = [&](const char* what) {
+        char b[64];
+        snprintf(b, sizeof b, " %s@%.0f", what,
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_call).count());
+        dbg_log += b;
+    };
     g_sync_us = 0.0;
     int iters_done = 0;
     const size_t len = p.nn();
@@ -150,8 +157,10 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
         cur = obj.eval(ctr, z.p, g.p);
     }
     if (plan_nonfinite(p, g.p, len)) raise(PTG_ERR_NUMERIC, "non-finite iterate in lbfgs");
+    if (lbfgs_debug()) dbg_mark("nonfinite");
     const double grad_floor = cfg.grad_tol_abs * (1.0 + dnorm(p, z0));
     const double g0 = dnorm(p, g.p);
+    if (lbfgs_debug()) dbg_mark("norms");
     double gnorm = g0;
     if (hist) hist->push_back({ctr.weighted, cur, gnorm});
     auto satisfied = [&](double gn) { return gn <= std::max(cfg.grad_tol_rel * g0, grad_floor); };
@@ -217,6 +226,7 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
         double* res_d = md_scratch + kMultiDotScratch;   // device image of res_h
         double* stats_d = res_d + 1;
         double* md_d = res_d + 9;
+        if (lbfgs_debug()) { PTG_CUDA(cudaStreamSynchronize(p.stream)); dbg_mark("ws"); }
         for (int iter = 1; iter <= cfg.max_iters; ++iter) {
             std::vector<const void*> sp, yp;
             std::vector<double> syv;
@@ -371,6 +381,7 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                 if (compact) node_launch(nc, p.stream);
                 lsr = d_linesearch(obj, z.p, dir.p, ctr, cfg.linesearch_max, &cur, nz.p, ng.p, stats);
             }
+            if (lbfgs_debug() && iter <= 2) dbg_mark("ls");
             if (lsr.stalled) {
                 out.reason = PTG_STOP_STALL;
                 break;
@@ -422,8 +433,8 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     PTG_CUDA(cudaStreamSynchronize(p.stream));
     if (lbfgs_debug() && iters_done > 0) {
         const double tot = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_call).count();
-        fprintf(stderr, "[lbfgs] n=%d iters %d: %.1f us/iter wall, %.1f us/iter in line-search syncs\n", p.n,
-                iters_done, tot / iters_done, g_sync_us / iters_done);
+        fprintf(stderr, "[lbfgs] n=%d iters %d: %.1f us/iter wall, %.1f us/iter in line-search syncs |%s\n", p.n,
+                iters_done, tot / iters_done, g_sync_us / iters_done, dbg_log.c_str());
     }
     return out;
 }
