@@ -12,6 +12,16 @@
 
 namespace ptg {
 
+// Programmatic dependent launch: wait until the preceding grid in the stream
+// has completed and flushed (no-op when launched without the PDL attribute),
+// then let the next grid start launching.
+__device__ __forceinline__ void pdl_wait_and_trigger() {
+#if defined(__CUDA_ARCH__)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 // Status-carrying exception used inside the library; the C-ABI layer
 // (capi.cu) converts it to an int status + ptg_last_error() string.
 struct Status : std::runtime_error {

@@ -99,6 +99,8 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
         mbar_init(&bar_a[f], 1);
         mbar_init(&bar_p[f], 1);
         fence_mbarrier_init();
+        // PDL (solver graphs): the object is the predecessor's output
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         if (live) {   // object window -> [M][S] tile (out-of-range columns zero-filled)
             mbar_arrive_expect_tx(&bar_z[f], M * S * sizeof(float2));
             tma_load_2d(fr, &tm_z, 2 * (pj.y - odd), pj.x, &bar_z[f]);
@@ -119,6 +121,9 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
         for (int r = 0; r < M; ++r) x[r] = __ldg(probe + r * M + t);
 #endif
     }
+    // the probe is immutable: its prefetch above may overlap the predecessor
+    // grid; nothing written by it is read or overwritten before this point
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     if (live) mbar_wait(&bar_z[f], 0);
     TL(1);

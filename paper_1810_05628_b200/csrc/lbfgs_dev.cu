@@ -311,6 +311,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_pair_stats(const cplx<T>* nz
                                                                double* scratch, double* out) {
     __shared__ double red[4][kReduceThreads / 32];
     __shared__ bool last;
+    pdl_wait_and_trigger();
     const size_t chunk = (len + kPsBlocks - 1) / kPsBlocks;
     const size_t lo = min(len, (size_t)blockIdx.x * chunk), hi = min(len, lo + chunk);
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -400,6 +401,7 @@ template <typename T>
 __global__ void __launch_bounds__(kReduceThreads) k_multi_dot(const MultiDotArgs<T> a) {
     using C = cplx<T>;
     __shared__ double red[kMdPairs * 4][kReduceThreads / 32];
+    pdl_wait_and_trigger();
     const size_t chunk = (a.len + kMdBlocks - 1) / kMdBlocks;
     const size_t lo = min(a.len, (size_t)blockIdx.x * chunk), hi = min(a.len, lo + chunk);
     const int p0 = blockIdx.y * kMdPairs;
@@ -436,6 +438,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_multi_dot(const MultiDotArgs
 // out[d] = fixed tree over partial[d][*], one block per product
 __global__ void __launch_bounds__(kReduceThreads) k_multi_sum(const double* partial, double* out) {
     __shared__ double red[kReduceThreads / 32];
+    pdl_wait_and_trigger();
     const double* pd = partial + (size_t)blockIdx.x * kMdBlocks;
     double t = 0.0;
     for (int i = threadIdx.x; i < kMdBlocks; i += kReduceThreads) t += pd[i];
@@ -467,6 +470,7 @@ struct CombineArgs {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_combine(const CombineArgs<T> a) {
+    pdl_wait_and_trigger();
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < a.len; i += (size_t)gridDim.x * blockDim.x) {
         const cplx<T> gv = a.g[i];
         double rx = a.gamma * (double)gv.x, ry = a.gamma * (double)gv.y;
@@ -729,7 +733,20 @@ void node_multi_dot(const Plan& p, const void* const* s, const void* const* y, i
 }
 
 void node_launch(const KNode& n, cudaStream_t s) {
-    PTG_CUDA(cudaLaunchKernel(n.prm.func, n.prm.gridDim, n.prm.blockDim, n.prm.kernelParams, n.prm.sharedMemBytes, s));
+    // programmatic dependent launch: the kernel's launch overlaps its
+    // predecessor's tail; every one of these kernels starts with
+    // griddepcontrol.wait, so nothing is read early
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = n.prm.gridDim;
+    cfg.blockDim = n.prm.blockDim;
+    cfg.dynamicSmemBytes = n.prm.sharedMemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PTG_CUDA(cudaLaunchKernelExC(&cfg, n.prm.func, n.prm.kernelParams));
     count_launch();
 }
 

@@ -177,7 +177,7 @@ bool tma_path_ok(const Plan& p) {
 
 template <int M, int OP, bool PROBE>
 void launch_tma_p(const FrameArgs<float>& a, int count, const CUtensorMap& tz, const CUtensorMap& ta,
-                  const CUtensorMap& tp, cudaStream_t s) {
+                  const CUtensorMap& tp, cudaStream_t s, bool pdl) {
     constexpr int FPC = tma_frames_per_cta<M>();
     constexpr size_t smem = tma_smem_bytes<M>();
     auto kern = frame_tma_kernel<M, OP, PROBE>;
@@ -186,7 +186,21 @@ void launch_tma_p(const FrameArgs<float>& a, int count, const CUtensorMap& tz, c
         PTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    kern<<<(count + FPC - 1) / FPC, M * FPC, smem, s>>>(a, count, tz, ta, tp);
+    if (!pdl) {
+        kern<<<(count + FPC - 1) / FPC, M * FPC, smem, s>>>(a, count, tz, ta, tp);
+    } else {   // solver graphs: launch (and the probe prefetch) overlap the predecessor
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((count + FPC - 1) / FPC);
+        cfg.blockDim = dim3(M * FPC);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        PTG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, count, tz, ta, tp));
+    }
     PTG_CHECK_LAUNCH();
 }
 
@@ -225,9 +239,9 @@ void launch_tma(Plan& p, const FrameArgs<float>& a, int count, const void* z, co
     const CUtensorMap& tp =
         pr ? *reinterpret_cast<const CUtensorMap*>(p.tm_probe_epi[OP == OP_INTENSITY ? 1 : 0]) : *tz;
     switch (p.M) {
-        case 16: pr ? launch_tma_p<16, OP, true>(a, count, *tz, ta, tp, p.stream) : launch_tma_p<16, OP, false>(a, count, *tz, ta, tp, p.stream); break;
-        case 32: pr ? launch_tma_p<32, OP, true>(a, count, *tz, ta, tp, p.stream) : launch_tma_p<32, OP, false>(a, count, *tz, ta, tp, p.stream); break;
-        default: pr ? launch_tma_p<64, OP, true>(a, count, *tz, ta, tp, p.stream) : launch_tma_p<64, OP, false>(a, count, *tz, ta, tp, p.stream); break;
+        case 16: pr ? launch_tma_p<16, OP, true>(a, count, *tz, ta, tp, p.stream, p.pdl_frames) : launch_tma_p<16, OP, false>(a, count, *tz, ta, tp, p.stream, p.pdl_frames); break;
+        case 32: pr ? launch_tma_p<32, OP, true>(a, count, *tz, ta, tp, p.stream, p.pdl_frames) : launch_tma_p<32, OP, false>(a, count, *tz, ta, tp, p.stream, p.pdl_frames); break;
+        default: pr ? launch_tma_p<64, OP, true>(a, count, *tz, ta, tp, p.stream, p.pdl_frames) : launch_tma_p<64, OP, false>(a, count, *tz, ta, tp, p.stream, p.pdl_frames); break;
     }
 }
 

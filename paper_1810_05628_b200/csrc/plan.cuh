@@ -146,6 +146,10 @@ struct Plan {
     int chunk_size = 0;
     std::vector<std::unique_ptr<Chunk>> chunks;
     int64_t launches = 0;
+    // the complex64 TMA frame kernel is launched with programmatic dependent
+    // launch (set by the solvers while they capture their iteration graphs;
+    // never for a timed standalone evaluation)
+    bool pdl_frames = false;
 
     ~Plan();
     size_t celem() const { return prec == PTG_C64 ? 8 : 16; }

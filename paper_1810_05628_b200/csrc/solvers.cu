@@ -330,13 +330,16 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                     try {
                         node_launch(nc, p.stream);                              // dir and nz = z + dir
                         ctr.record(obj.level, obj.weight);                      // charge before evaluating
+                        p.pdl_frames = true;
                         plan_eval(p, obj.metric, nz.p, obj.v, ng.p, res_d);     // value -> res_d[0]
+                        p.pdl_frames = false;
                         node_launch(nps, p.stream);                             // -> res_d[1..5]
                         node_launch(nmd, p.stream);
                         node_launch(nms, p.stream);                             // -> res_d[9..]
                         PTG_CUDA(cudaMemcpyAsync(res_h.p, res_d, kRes * sizeof(double), cudaMemcpyDeviceToHost,
                                                  p.stream));
                     } catch (...) {
+                        p.pdl_frames = false;
                         cudaStreamEndCapture(p.stream, &gr);
                         if (gr) cudaGraphDestroy(gr);
                         throw;
