@@ -64,7 +64,8 @@ __device__ __forceinline__ void dft_q(float2* v) {
 
 template <int Q, int L, int OP, bool PROBE>
 __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
-    frame_cl_kernel(FrameArgs<float> a, const float* __restrict__ amp_perm, const float2* __restrict__ tw_g) {
+    frame_cl_kernel(FrameArgs<float> a, const float* __restrict__ amp_perm, const float2* __restrict__ tw_g,
+                    const float2* __restrict__ probe_epi) {
     namespace cg = cooperative_groups;
     constexpr int M = Q * L, NT = M, PM = cl_pitch<Q, L>(), NPC = L / Q, AP = cl_amp_pitch<Q, L>();
     cg::cluster_group cl = cg::this_cluster();
@@ -243,12 +244,13 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
             for (int k = 0; k < L; ++k) rb[k / NPC][((k % NPC) * Q + q) * PM + t] = x[k];
         }
     }
-    // epilogue probe values (rows q NPC + i + 64 s, column t) in flight across the barrier
+    // epilogue probe values conj(sc P) (rows q NPC + i + L s, column t) in
+    // flight across the barrier
     if constexpr (PROBE) {
 #pragma unroll
         for (int i = 0; i < NPC; ++i)
 #pragma unroll
-            for (int s = 0; s < Q; ++s) x[i * Q + s] = __ldg(a.probe + (size_t)(q * NPC + i + L * s) * M + t);
+            for (int s = 0; s < Q; ++s) x[i * Q + s] = __ldg(probe_epi + (size_t)(q * NPC + i + L * s) * M + t);
     }
 
     // per-CTA misfit partial (fixed shuffle tree + fixed warp order)
@@ -268,10 +270,22 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         if constexpr (MPP > Q) a.misfit[(size_t)j * MPP + Q + q] = 0.0;
     }
 
-    // column DIT combine over the cluster + epilogue: rows r + 64 s, column t
+    // column DIT combine over the cluster + epilogue: rows r + L s, column t.
+    // One base pointer per CTA and 32-bit row offsets (rows r + L s of this
+    // CTA, r = q NPC + i); stash rows have pitch SP with the window at
+    // column (col0 & 1) and two zero pads (plan.cuh), written once below.
     const float sc = (OP == OP_DISTANCE) ? 1.f / (float(M) * float(M)) : 2.f;
     const int odd = pj.y & 1;
     constexpr int SP = stash_pitch(M);
+    float2* __restrict__ base;
+    unsigned rs;
+    if (a.planes) {
+        base = a.planes + (size_t)a.color[j] * n * n + (size_t)(pj.x + q * NPC) * n + pj.y + t;
+        rs = (unsigned)n;
+    } else {
+        base = a.stash + (size_t)j * M * SP + (size_t)(q * NPC) * SP + odd + t;
+        rs = (unsigned)SP;
+    }
 #pragma unroll   // x[] is indexed by i: full unroll keeps it in registers
     for (int i = 0; i < NPC; ++i) {
         const int r = q * NPC + i;
@@ -283,19 +297,14 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         dft_q<Q>(v);
 #pragma unroll
         for (int s = 0; s < Q; ++s) {
-            const int row = r + L * s;
-            const float2 val = PROBE ? epi_contrib(v[s], x[i * Q + s], sc) : epi_contrib(v[s], sc);
-            if (a.planes) {
-                a.planes[(size_t)a.color[j] * n * n + (size_t)(pj.x + row) * n + pj.y + t] = val;
-            } else {
-                float2* out = a.stash + (size_t)j * M * SP + (size_t)row * SP;
-                out[odd + t] = val;
-                if (t == 0) {   // the row's two zero pads (plan.cuh stash layout)
-                    out[odd ? 0 : M] = make_float2(0.f, 0.f);
-                    out[M + 1] = make_float2(0.f, 0.f);
-                }
-            }
+            const float2 val = PROBE ? epi_contrib_pre(v[s], x[i * Q + s]) : epi_contrib(v[s], sc);
+            base[(unsigned)(i + L * s) * rs] = val;
         }
+    }
+    if (!a.planes && t < 2 * NPC * Q) {   // the zero pads of this CTA's stash rows
+        const int k = t >> 1, row = q * NPC + k % NPC + L * (k / NPC);
+        float2* out = a.stash + (size_t)j * M * SP + (size_t)row * SP;
+        out[(t & 1) ? M + 1 : (odd ? 0 : M)] = make_float2(0.f, 0.f);
     }
     TL(5);
 }

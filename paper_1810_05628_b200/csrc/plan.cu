@@ -170,6 +170,23 @@ __global__ void k_scale_conj_c64(float2* __restrict__ out, const float2* __restr
     if (i < n) out[i] = make_float2(in[i].x * sc, -(in[i].y * sc));
 }
 
+// conj(sc * P) per metric (sc = 1/M^2 distance, 2 intensity: powers of two,
+// so the table is exact), read by the complex64 epilogues: the contribution
+// is then one packed complex multiply.  [0] distance, [1] intensity.
+const float2* probe_epi_table(Plan& p, int op) {
+    if (!p.probe_epi.p) {
+        p.probe_epi.alloc(2 * p.MM() * sizeof(float2));
+        float2* pe = p.probe_epi.as<float2>();
+        const float sc[2] = {1.f / ((float)p.M * (float)p.M), 2.f};
+        for (int k = 0; k < 2; ++k) {
+            k_scale_conj_c64<<<(unsigned)((p.MM() + 255) / 256), 256, 0, p.stream>>>(
+                pe + k * p.MM(), p.probe.as<const float2>(), sc[k], p.MM());
+            PTG_CHECK_LAUNCH();
+        }
+    }
+    return p.probe_epi.as<const float2>() + (op == OP_INTENSITY ? p.MM() : 0);
+}
+
 bool tma_path_ok(const Plan& p) {
     return p.prec == PTG_C64 && (p.M == 16 || p.M == 32 || p.M == 64) && p.w == p.M && p.n % 2 == 0 &&
            p.N > 0;
@@ -222,18 +239,10 @@ void launch_tma(Plan& p, const FrameArgs<float>& a, int count, const void* z, co
     }
     const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(p.tm_amp);
     const bool pr = a.probe != nullptr;
-    if (pr && !p.tm_probe_ok) {
-        // the epilogue reads conj(sc * P) (sc = 1/M^2 distance, 2 intensity:
-        // powers of two, so the table is exact): M x M complex64 as float32 [M][2M], one box
-        p.probe_epi.alloc(2 * p.MM() * sizeof(float2));
-        float2* pe = p.probe_epi.as<float2>();
-        const float sc[2] = {1.f / ((float)p.M * (float)p.M), 2.f};
-        for (int k = 0; k < 2; ++k) {
-            k_scale_conj_c64<<<(unsigned)((p.MM() + 255) / 256), 256, 0, p.stream>>>(
-                pe + k * p.MM(), p.probe.as<const float2>(), sc[k], p.MM());
-            PTG_CHECK_LAUNCH();
+    if (pr && !p.tm_probe_ok) {   // M x M complex64 as float32 [M][2M], one box
+        const float2* pe = probe_epi_table(p, 0);
+        for (int k = 0; k < 2; ++k)
             encode_z(reinterpret_cast<CUtensorMap*>(p.tm_probe_epi[k]), pe + k * p.MM(), p.M, p.M, 0);
-        }
         p.tm_probe_ok = true;
     }
     const CUtensorMap& tp =
@@ -303,7 +312,8 @@ void launch_cl_t(Plan& p, const FrameArgs<float>& a, int count, const float* amp
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    PTG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, amp_perm, tw));
+    const float2* pe = PROBE ? probe_epi_table(p, OP) : nullptr;
+    PTG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, amp_perm, tw, pe));
 }
 
 template <int Q, int L, int OP>
