@@ -107,8 +107,6 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
     // r = q NPC + i (window rows r + 64 s, column t) straight from global memory
     // and stores output s into CTA s's row r
     float2 x[L];
-    __syncthreads();                                              // twiddle table
-    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");   // every CTA of the cluster runs
     {
         // batches of BT butterflies: their Q z values and probe values in flight together
         constexpr int BT = 16 / Q;
@@ -124,6 +122,13 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                     zv[i * Q + s] = zc[(size_t)row * n];
                     if constexpr (PROBE) pv[i * Q + s] = __ldg(a.probe + (size_t)row * M + t);
                 }
+            if (b == 0) {
+                // the first batch's loads are in flight across the twiddle-table
+                // sync and the cluster start handshake (needed only before the
+                // first remote store)
+                __syncthreads();                                              // twiddle table
+                asm volatile("barrier.cluster.wait.aligned;" ::: "memory");   // every CTA of the cluster runs
+            }
 #pragma unroll
             for (int i = 0; i < BT; ++i) {
                 const int r = q * NPC + b + i;
