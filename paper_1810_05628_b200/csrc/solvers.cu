@@ -3,6 +3,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "solvers.cuh"
@@ -156,11 +157,28 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     } else {
         cur = obj.eval(ctr, z.p, g.p);
     }
-    if (plan_nonfinite(p, g.p, len)) raise(PTG_ERR_NUMERIC, "non-finite iterate in lbfgs");
-    if (lbfgs_debug()) dbg_mark("nonfinite");
-    const double grad_floor = cfg.grad_tol_abs * (1.0 + dnorm(p, z0));
-    const double g0 = dnorm(p, g.p);
-    if (lbfgs_debug()) dbg_mark("norms");
+    // isFinite(g), |z0|^2 and |g|^2 enqueued together, read back after one
+    // synchronisation (same kernels and partitions as plan_nonfinite / dnorm)
+    double z0sq = 0.0, gsq = 0.0;
+    {
+        p.hval.ensure(8 * sizeof(double));
+        double* hv = p.hval.as<double>();
+        double* vd = p.value.as<double>();
+        dev_nonfinite(p.prec, g.p, len, p.flag.as<int>(), p.stream);
+        dev_dot(p.prec, z0, z0, len, p.scratch.as<double>(), vd + 1, p.stream);
+        dev_dot(p.prec, g.p, g.p, len, p.scratch.as<double>(), vd + 2, p.stream);
+        PTG_CUDA(cudaMemcpyAsync(hv + 4, vd + 1, 2 * sizeof(double), cudaMemcpyDeviceToHost, p.stream));
+        PTG_CUDA(cudaMemcpyAsync(hv + 6, p.flag.p, sizeof(int), cudaMemcpyDeviceToHost, p.stream));
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+        int bad = 0;
+        std::memcpy(&bad, hv + 6, sizeof(int));
+        if (bad) raise(PTG_ERR_NUMERIC, "non-finite iterate in lbfgs");
+        z0sq = hv[4];
+        gsq = hv[5];
+    }
+    if (lbfgs_debug()) dbg_mark("nonfinite+norms");
+    const double grad_floor = cfg.grad_tol_abs * (1.0 + std::sqrt(z0sq));
+    const double g0 = std::sqrt(gsq);
     double gnorm = g0;
     if (hist) hist->push_back({ctr.weighted, cur, gnorm});
     auto satisfied = [&](double gn) { return gn <= std::max(cfg.grad_tol_rel * g0, grad_floor); };
@@ -605,7 +623,6 @@ double d_mgopt_cycle(Hier& h, int level, const void* z, const void* v, Counter& 
     // plain fine gradient = shifted gradient + v
     if (v) dev_add_scaled(p.prec, gfine.p, gbar.p, 1.0, v, len, p.stream);
     else dev_copy(p.prec, gfine.p, gbar.p, len, p.stream);
-    PTG_CUDA(cudaStreamSynchronize(p.stream));
     DObj coarse_plain = level_obj(h, level + 1, nullptr);
     const double cval = coarse_plain.eval(ctr, zBarH.p, cg.p);
     // vH = R(v) + grad phi_H(zBarH) - R(grad phi_h(zBar))   (multigrid.cpp:142-147)
@@ -626,7 +643,7 @@ double d_mgopt_cycle(Hier& h, int level, const void* z, const void* v, Counter& 
 
     dev_sub(pc.prec, tmpH.p, zrec.p, zBarH.p, lenH, pc.stream);
     dev_prolong_field(pc.prec, tmpH.p, pc.n, corr.p, pc.stream);
-    PTG_CUDA(cudaStreamSynchronize(pc.stream));
+    if (pc.stream != p.stream) PTG_CUDA(cudaStreamSynchronize(pc.stream));
     LsOut lsr = d_linesearch(obj, zbar.p, corr.p, ctr, h.opt.linesearch_max, &vbar, zplus.p, gplus.p);
     double pval = lsr.value;
     if (lsr.stalled) {
