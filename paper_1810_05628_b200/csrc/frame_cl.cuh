@@ -54,6 +54,22 @@ __host__ __device__ constexpr size_t cl_smem_bytes() {
 template <int Q, int L>
 __host__ __device__ constexpr int cl_min_blocks() { return L == 32 ? (Q == 4 ? 4 : 2) : Q == 2 ? 2 : 1; }
 
+#ifndef PTG_CL_ASYNC_GATHER
+#define PTG_CL_ASYNC_GATHER 1
+#endif
+// shared::cta address -> the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+// 8-byte remote store completing 8 tx bytes on the receiver's mbarrier
+__device__ __forceinline__ void st_async_f2(uint32_t raddr, float2 v, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "f"(v.x), "f"(v.y), "r"(rbar)
+                 : "memory");
+}
+
 // forward DFT_Q in place, natural order
 template <int Q>
 __device__ __forceinline__ void dft_q(float2* v) {
@@ -80,10 +96,22 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
     const int t = threadIdx.x;
     const int2 pj = a.pos[j];
     const int n = a.n;
-    // cluster start handshake, split: the wait sits before the first remote store
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     float* amp_s = reinterpret_cast<float*>(tw + M);   // [L][M + 4] (staged variants)
     __shared__ __align__(8) unsigned long long bar_a;
+#if PTG_CL_ASYNC_GATHER
+    // gather exchange by st.async: every CTA's L x M rows arrive as remote
+    // stores that complete_tx on the receiver's mbarrier (no cluster barrier,
+    // no fence); initialised before the cluster start handshake below
+    __shared__ __align__(8) unsigned long long bar_g;
+    if (t == 0) {
+        mbar_init(&bar_g, 1);
+        fence_mbarrier_init();
+        mbar_arrive_expect_tx(&bar_g, (uint32_t)(L * M * sizeof(float2)));
+    }
+    __syncthreads();
+#endif
+    // cluster start handshake, split: the wait sits before the first remote store
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
     if constexpr (cl_amp_staged<Q, L>()) {
         if (t == 0) {
             mbar_init(&bar_a, 1);
@@ -138,12 +166,22 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                 dft_q<Q>(v);
 #pragma unroll
                 for (int s = 1; s < Q; ++s) v[s] = cmul(tw[r * s], v[s]);
+#if PTG_CL_ASYNC_GATHER
+#pragma unroll
+                for (int s = 0; s < Q; ++s)
+                    st_async_f2(mapa_u32(smem_u32(buf + r * PM + t), s), v[s], mapa_u32(smem_u32(&bar_g), s));
+#else
 #pragma unroll
                 for (int s = 0; s < Q; ++s) rb[s][r * PM + t] = v[s];
+#endif
             }
         }
     }
+#if PTG_CL_ASYNC_GATHER
+    mbar_wait(&bar_g, 0);   // all Q senders' rows have landed in this CTA
+#else
     cl.sync();
+#endif
     TL(1);
 
     // row-stage roles: butterflies (row g + Q i, element m); FFT64 quarter-rows (rr, qq)
