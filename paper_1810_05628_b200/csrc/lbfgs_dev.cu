@@ -395,6 +395,12 @@ struct MultiDotArgs {
     int A;
     size_t len;
     double* partial;   // [4 A][kMdBlocks]
+    // optional (zn != nullptr): the newest pair (a = A - 1) and yc are formed
+    // in-kernel as s = zn - zo, y = yc = gn - go (k_pair_stats' arithmetic), so
+    // this kernel need not wait for k_pair_stats to store them
+    const cplx<T>* zn;
+    const cplx<T>* zo;
+    const cplx<T>* go;
 };
 
 template <typename T>
@@ -409,11 +415,14 @@ __global__ void __launch_bounds__(kReduceThreads) k_multi_dot(const MultiDotArgs
 #pragma unroll
     for (int k = 0; k < kMdPairs * 4; ++k) acc[k] = 0.0;
     for (size_t i = lo + threadIdx.x; i < hi; i += kReduceThreads) {
-        const C yc = a.yc[i], gn = a.gn[i];
+        const C gn = a.gn[i];
+        const C yc = a.zn ? csub(gn, a.go[i]) : a.yc[i];
 #pragma unroll
         for (int q = 0; q < kMdPairs; ++q) {
             if (p0 + q < a.A) {
-                const C sv = a.s[p0 + q][i], yv = a.y[p0 + q][i];
+                const bool fresh = a.zn && p0 + q == a.A - 1;
+                const C sv = fresh ? csub(a.zn[i], a.zo[i]) : a.s[p0 + q][i];
+                const C yv = fresh ? yc : a.y[p0 + q][i];
                 acc[4 * q + 0] = __dadd_rn(acc[4 * q + 0], dot_term(sv, yc));
                 acc[4 * q + 1] = __dadd_rn(acc[4 * q + 1], dot_term(yv, yc));
                 acc[4 * q + 2] = __dadd_rn(acc[4 * q + 2], dot_term(sv, gn));
@@ -514,6 +523,7 @@ void multi_dot_t(const Plan& p, const void* const* s, const void* const* y, int 
     a.A = A;
     a.len = p.nn();
     a.partial = scratch;
+    a.zn = a.zo = a.go = nullptr;
     k_multi_dot<T><<<dim3(kMdBlocks, (A + kMdPairs - 1) / kMdPairs), kReduceThreads, 0, p.stream>>>(a);
     k_multi_sum<<<4 * A, kReduceThreads, 0, p.stream>>>(scratch, out_dev);
     PTG_CHECK_LAUNCH();
@@ -673,8 +683,12 @@ struct PairStatsArgs {
 };
 template <typename T>
 void node_multi_dot_t(const Plan& p, const void* const* s, const void* const* y, int A, const void* yc,
-                      const void* gn, double* scratch, double* out_dev, KNode& md, KNode& ms) {
+                      const void* gn, double* scratch, double* out_dev, KNode& md, KNode& ms, const void* zn,
+                      const void* zo, const void* go) {
     MultiDotArgs<T>& a = node_store<MultiDotArgs<T>>(md);
+    a.zn = static_cast<const cplx<T>*>(zn);
+    a.zo = static_cast<const cplx<T>*>(zo);
+    a.go = static_cast<const cplx<T>*>(go);
     for (int i = 0; i < A; ++i) {
         a.s[i] = static_cast<const cplx<T>*>(s[i]);
         a.y[i] = static_cast<const cplx<T>*>(y[i]);
@@ -726,10 +740,11 @@ void node_pair_stats(const Plan& p, const void* nz, const void* z, const void* n
 }
 
 void node_multi_dot(const Plan& p, const void* const* s, const void* const* y, int A, const void* yc,
-                    const void* gn, double* scratch, double* out_dev, KNode& md, KNode& ms) {
+                    const void* gn, double* scratch, double* out_dev, KNode& md, KNode& ms, const void* zn,
+                    const void* zo, const void* go) {
     if (A <= 0 || A > kMaxPairs + 1) raise(PTG_ERR_INTERNAL, "multi_dot: pair count");
-    if (p.prec == PTG_C64) node_multi_dot_t<float>(p, s, y, A, yc, gn, scratch, out_dev, md, ms);
-    else node_multi_dot_t<double>(p, s, y, A, yc, gn, scratch, out_dev, md, ms);
+    if (p.prec == PTG_C64) node_multi_dot_t<float>(p, s, y, A, yc, gn, scratch, out_dev, md, ms, zn, zo, go);
+    else node_multi_dot_t<double>(p, s, y, A, yc, gn, scratch, out_dev, md, ms, zn, zo, go);
 }
 
 void node_launch(const KNode& n, cudaStream_t s) {

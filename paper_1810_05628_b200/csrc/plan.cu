@@ -35,6 +35,9 @@ Plan::~Plan() {
     }
     if (hg.exec) cudaGraphExecDestroy(hg.exec);
     for (auto e : ev_band) cudaEventDestroy(e);
+    if (ev_side[0]) cudaEventDestroy(ev_side[0]);
+    if (ev_side[1]) cudaEventDestroy(ev_side[1]);
+    if (s_side) cudaStreamDestroy(s_side);
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
     if (own_stream) cudaStreamDestroy(own_stream);

@@ -76,6 +76,9 @@ struct Plan {
     cudaStream_t stream = nullptr;
     // banded host evaluation (plan_eval_host): copy-in / copy-out streams + events
     cudaStream_t s_in = nullptr, s_out = nullptr;
+    // solver graphs: side stream + fork/join events (d_lbfgs products)
+    cudaStream_t s_side = nullptr;
+    cudaEvent_t ev_side[2] = {nullptr, nullptr};
     std::vector<cudaEvent_t> ev_band;
     DevMem stage_out;
     // the banded host evaluation replayed as one CUDA graph (pinned host

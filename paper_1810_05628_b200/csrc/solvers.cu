@@ -13,7 +13,8 @@ namespace ptg {
 
 // PTG_LBFGS_DEBUG=1: host time inside the line-search synchronisations vs the
 // whole LBFGS call (dev instrumentation)
-static double g_sync_us = 0.0;
+static double g_sync_us = 0.0, g_graph_us = 0.0;
+static int g_graph_n = 0;
 static bool lbfgs_debug() {
     static const bool on = getenv("PTG_LBFGS_DEBUG") != nullptr;
     return on;
@@ -146,6 +147,8 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
         dbg_log += b;
     };
     g_sync_us = 0.0;
+    g_graph_us = 0.0;
+    g_graph_n = 0;
     int iters_done = 0;
     const size_t len = p.nn();
     DVec z(p, len), g(p, len), dir(p, len), nz(p, len), ng(p, len);
@@ -232,6 +235,14 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
         }
     } ig[2];
     static const bool use_graph = !(getenv("PTG_LBFGS_GRAPH") && getenv("PTG_LBFGS_GRAPH")[0] == '0');
+    // fork/join resources of the captured iteration (the plan's side stream)
+    if (use_graph && !p.s_side) {
+        PTG_CUDA(cudaStreamCreateWithFlags(&p.s_side, cudaStreamNonBlocking));
+        PTG_CUDA(cudaEventCreateWithFlags(&p.ev_side[0], cudaEventDisableTiming));
+        PTG_CUDA(cudaEventCreateWithFlags(&p.ev_side[1], cudaEventDisableTiming));
+    }
+    cudaStream_t side = p.s_side;
+    cudaEvent_t* ig_ev = p.ev_side;
     if (satisfied(gnorm)) {
         out.reason = PTG_STOP_TOLERANCE;
     } else {
@@ -318,7 +329,10 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
             myp.push_back(pr.y.p);
             if (compact) {
                 node_pair_stats(p, nz.p, z.p, ng.p, g.p, pr.s.p, pr.y.p, wsd, stats_d, nps);
-                node_multi_dot(p, msp.data(), myp.data(), k + 1, pr.y.p, ng.p, md_scratch, md_d, nmd, nms);
+                // the products form the new pair themselves: independent of the
+                // pair statistics kernel (the graph runs the two concurrently)
+                node_multi_dot(p, msp.data(), myp.data(), k + 1, pr.y.p, ng.p, md_scratch, md_d, nmd, nms, nz.p,
+                               z.p, g.p);
             }
             auto stats = [&]() {
                 if (compact) {
@@ -351,9 +365,14 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                         p.pdl_frames = true;
                         plan_eval(p, obj.metric, nz.p, obj.v, ng.p, res_d);     // value -> res_d[0]
                         p.pdl_frames = false;
+                        // fork: products on a side stream, pair statistics here
+                        PTG_CUDA(cudaEventRecord(ig_ev[0], p.stream));
+                        PTG_CUDA(cudaStreamWaitEvent(side, ig_ev[0], 0));
+                        node_launch(nmd, side);
+                        node_launch(nms, side);                                 // -> res_d[9..]
+                        PTG_CUDA(cudaEventRecord(ig_ev[1], side));
                         node_launch(nps, p.stream);                             // -> res_d[1..5]
-                        node_launch(nmd, p.stream);
-                        node_launch(nms, p.stream);                             // -> res_d[9..]
+                        PTG_CUDA(cudaStreamWaitEvent(p.stream, ig_ev[1], 0));   // join
                         PTG_CUDA(cudaMemcpyAsync(res_h.p, res_d, kRes * sizeof(double), cudaMemcpyDeviceToHost,
                                                  p.stream));
                     } catch (...) {
@@ -391,11 +410,25 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                     ctr.record(obj.level, obj.weight);   // charge before evaluating (solvers.hpp:33-36)
                     p.launches += G.launches;
                 }
+                static cudaEvent_t dbg_ev[2] = {nullptr, nullptr};
+                if (lbfgs_debug()) {
+                    if (!dbg_ev[0]) {
+                        PTG_CUDA(cudaEventCreate(&dbg_ev[0]));
+                        PTG_CUDA(cudaEventCreate(&dbg_ev[1]));
+                    }
+                    PTG_CUDA(cudaEventRecord(dbg_ev[0], p.stream));
+                }
                 PTG_CUDA(cudaGraphLaunch(G.exec, p.stream));
+                if (lbfgs_debug()) PTG_CUDA(cudaEventRecord(dbg_ev[1], p.stream));
                 const auto ts = std::chrono::steady_clock::now();
                 PTG_CUDA(cudaStreamSynchronize(p.stream));
-                if (lbfgs_debug())
+                if (lbfgs_debug()) {
                     g_sync_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - ts).count();
+                    float ms = 0.f;
+                    cudaEventElapsedTime(&ms, dbg_ev[0], dbg_ev[1]);
+                    g_graph_us += ms * 1e3;
+                    ++g_graph_n;
+                }
                 lsr = d_linesearch_continue(obj, z.p, dir.p, ctr, cfg.linesearch_max, cur, nz.p, ng.p,
                                             res_h.as<double>()[0]);
             } else {
@@ -454,8 +487,9 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     PTG_CUDA(cudaStreamSynchronize(p.stream));
     if (lbfgs_debug() && iters_done > 0) {
         const double tot = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_call).count();
-        fprintf(stderr, "[lbfgs] n=%d iters %d: %.1f us/iter wall, %.1f us/iter in line-search syncs |%s\n", p.n,
-                iters_done, tot / iters_done, g_sync_us / iters_done, dbg_log.c_str());
+        fprintf(stderr, "[lbfgs] n=%d iters %d: %.1f us/iter wall, %.1f us/iter in line-search syncs, graph %.1f us GPU |%s\n",
+                p.n, iters_done, tot / iters_done, g_sync_us / iters_done, g_graph_n ? g_graph_us / g_graph_n : 0.0,
+                dbg_log.c_str());
     }
     return out;
 }

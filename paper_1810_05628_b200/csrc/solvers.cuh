@@ -133,8 +133,11 @@ void node_combine(const Plan& p, const void* const* s, const void* const* y, con
                   void* trial = nullptr);
 void node_pair_stats(const Plan& p, const void* nz, const void* z, const void* ng, const void* g, void* s_out,
                      void* y_out, double* scratch, double* out_dev, KNode& n);
+// zn / zo / go (optional): form the newest pair (s = zn - zo, y = gn - go) and
+// yc in-kernel instead of reading what dev_pair_stats stores (no dependency)
 void node_multi_dot(const Plan& p, const void* const* s, const void* const* y, int A, const void* yc,
-                    const void* gn, double* scratch, double* out_dev, KNode& md, KNode& ms);
+                    const void* gn, double* scratch, double* out_dev, KNode& md, KNode& ms,
+                    const void* zn = nullptr, const void* zo = nullptr, const void* go = nullptr);
 void node_launch(const KNode& n, cudaStream_t s);
 
 // solvers.cpp:87-141.  warm_g (device) with *warm_value, or null to evaluate.
