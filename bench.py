@@ -377,12 +377,15 @@ def run_ours(args):
     gh = torch.empty(cfg.n, cfg.n, dtype=torch.complex128).pin_memory().numpy()
     h2d = zh.nbytes
     d2h = gh.nbytes + 8
-    for _ in range(2):
+    # warm-up: the first call with these buffers runs eagerly, the second
+    # captures the replay graph; a few more settle clocks and caches
+    for _ in range(10):
         plan.evaluate(zh, out=gh) if world == 1 else None
+    e2e_steps = max(args.steps, 100)
     if world == 1:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(e2e_steps):
             plan.evaluate(zh, out=gh)
         e2e_s = time.perf_counter() - t0
     else:
@@ -390,7 +393,7 @@ def run_ours(args):
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(e2e_steps):
             zt.copy_(torch.from_numpy(zh).to(cdt), non_blocking=False)
             plan.evaluate_device(zt, grad, value_dev=val, sync_value=False)
             exchange(grad, val)
@@ -400,8 +403,8 @@ def run_ours(args):
         tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
-    e2e = {"value": total_patterns * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s / args.steps * 1e3,
+    e2e = {"value": total_patterns * e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s / e2e_steps * 1e3, "steps": e2e_steps,
            "api": "Plan.evaluate (ptg_eval): pinned complex128 z in, value + complex128 gradient out"}
 
     extras = {}
