@@ -234,7 +234,7 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
             if (graph) cudaGraphDestroy(graph);
         }
     } ig[2];
-    static const bool use_graph = !(getenv("PTG_LBFGS_GRAPH") && getenv("PTG_LBFGS_GRAPH")[0] == '0');
+    const bool use_graph = !(getenv("PTG_LBFGS_GRAPH") && getenv("PTG_LBFGS_GRAPH")[0] == '0');
     // fork/join resources of the captured iteration (the plan's side stream)
     if (use_graph && !p.s_side) {
         PTG_CUDA(cudaStreamCreateWithFlags(&p.s_side, cudaStreamNonBlocking));

@@ -216,3 +216,19 @@ def test_compact_lbfgs_matches_two_loop(oracle, monkeypatch):
     assert a.weighted_evals == b.weighted_evals and a.reason == b.reason
     np.testing.assert_allclose(a.history, b.history, rtol=1e-10)
     assert rel_l2(a.final_iterate, b.final_iterate) <= 1e-10
+
+
+@pytest.mark.parametrize("precision", ["c64", "c128"])
+def test_graph_replayed_lbfgs_matches_eager(oracle, monkeypatch, precision):
+    """From the third iteration the compact LBFGS iteration is replayed as a
+    CUDA graph (direction with the fused first trial, evaluation, statistics
+    and products on a side stream); the trajectory is bitwise the eager one."""
+    p, plan, cfg = _patch(oracle, precision)
+    z0 = np.ones((cfg.n, cfg.n), np.complex128)
+    a = plan.lbfgs(z0, max_iters=30, lbfgs_memory=5)
+    monkeypatch.setenv("PTG_LBFGS_GRAPH", "0")
+    b = plan.lbfgs(z0, max_iters=30, lbfgs_memory=5)
+    assert len(a.history) > 6
+    assert a.weighted_evals == b.weighted_evals and a.reason == b.reason
+    assert np.array_equal(a.history, b.history)
+    assert np.array_equal(a.final_iterate, b.final_iterate)
