@@ -8,6 +8,7 @@
 // reproducible run to run); the 11-tap Gaussian filters keep the reference's
 // per-sample order (s += g[j] * in[c + j], separately rounded), so the five
 // filtered maps match the reference to the last bit given the same inputs.
+#include <mutex>
 #include <cmath>
 
 #include "blas.cuh"
@@ -200,9 +201,13 @@ __global__ void k_sum_blocks(const double* partial, int nb, double* out) {
     }
 }
 
-void upload_gauss() {
-    static bool done = false;
-    if (done) return;
+void upload_gauss() {   // __constant__ memory is per device: once per device
+    static std::mutex mu;
+    static bool done[64] = {};
+    int dev = 0;
+    PTG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if (dev >= 0 && dev < 64 && done[dev]) return;
     double g[kWin], sum = 0.0;   // metrics.cpp:22-33
     for (int i = 0; i < kWin; ++i) {
         const double x = i - kWin / 2;
@@ -211,7 +216,7 @@ void upload_gauss() {
     }
     for (double& v : g) v /= sum;
     PTG_CUDA(cudaMemcpyToSymbol(c_gauss, g, sizeof g));
-    done = true;
+    if (dev >= 0 && dev < 64) done[dev] = true;
 }
 
 template <typename T>

@@ -15,6 +15,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <set>
 
 #include <cudaTypedefs.h>
 
@@ -90,16 +92,27 @@ constexpr int frame_threads() {
     return M <= 8 ? 32 : M == 16 ? 64 : M == 32 ? 128 : M == 64 ? 256 : 512;
 }
 
+// opt-in dynamic shared memory above 48 KB, once per kernel and device (the
+// attribute is per device; one process may drive plans on several devices)
+template <class K>
+void set_smem_attr(K kern, size_t smem) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;   // (kernel, device)
+    int dev = 0;
+    PTG_CUDA(cudaGetDevice(&dev));
+    const std::pair<const void*, int> key{reinterpret_cast<const void*>(kern), dev};
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count(key)) return;
+    PTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    done.insert(key);
+}
+
 template <typename T, int M, int OP>
 void launch_frame_t(const FrameArgs<T>& a, int count, cudaStream_t s) {
     constexpr int NT = frame_threads<M>();
     const size_t smem = frame_smem_bytes<T, M>(NT);
     auto kern = frame_kernel<T, M, NT, OP>;
-    static bool attr = false;
-    if (!attr) {
-        PTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    set_smem_attr(kern, smem);
     kern<<<count, NT, smem, s>>>(a);
     PTG_CHECK_LAUNCH();
 }
@@ -201,11 +214,7 @@ void launch_tma_p(const FrameArgs<float>& a, int count, const CUtensorMap& tz, c
     constexpr int FPC = tma_frames_per_cta<M>();
     constexpr size_t smem = tma_smem_bytes<M>();
     auto kern = frame_tma_kernel<M, OP, PROBE>;
-    static bool attr = false;
-    if (!attr) {
-        PTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    set_smem_attr(kern, smem);
     if (!pdl) {
         kern<<<(count + FPC - 1) / FPC, M * FPC, smem, s>>>(a, count, tz, ta, tp);
     } else {   // solver graphs: launch (and the probe prefetch) overlap the predecessor
@@ -298,11 +307,7 @@ template <int Q, int L, int OP, bool PROBE>
 void launch_cl_t(Plan& p, const FrameArgs<float>& a, int count, const float* amp_perm, const float2* tw) {
     constexpr size_t smem = cl_smem_bytes<Q, L>();
     auto kern = frame_cl_kernel<Q, L, OP, PROBE>;
-    static bool attr = false;
-    if (!attr) {
-        PTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    set_smem_attr(kern, smem);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)count * Q);
     cfg.blockDim = dim3(Q * L);
@@ -372,14 +377,9 @@ template <typename T, int M, int OP>
 void launch_mp_t(Plan& p, const FrameArgs<T>& a, int first, int count, int which) {
     constexpr size_t smem = mp_smem_bytes<T, M>();
     constexpr int NT = mp_threads<M>();
-    static bool attr = false;
-    if (!attr) {
-        PTG_CUDA(cudaFuncSetAttribute(mp_rows_fwd<T, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        PTG_CUDA(cudaFuncSetAttribute(mp_cols<T, M, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        if constexpr (OP != OP_SIMULATE)
-            PTG_CUDA(cudaFuncSetAttribute(mp_rows_inv<T, M, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    set_smem_attr(mp_rows_fwd<T, M>, smem);
+    set_smem_attr(mp_cols<T, M, OP>, smem);
+    if constexpr (OP != OP_SIMULATE) set_smem_attr(mp_rows_inv<T, M, OP>, smem);
     MpArgs m{first, M / kMpLines, p.misfit.as<double>()};
     cplx<T>* scratch = p.mp_scratch.as<cplx<T>>();
     const dim3 grid(count, M / kMpLines);
@@ -780,11 +780,7 @@ void launch_pie_t(Plan& p, void* z, const void* wgt, double damping) {
     constexpr int NT = pie_threads<M>();
     const size_t smem = sizeof(cplx<T>) * ((size_t)M * frame_stride(M) + M);
     auto kern = k_pie_sweep<T, M, NT>;
-    static bool attr = false;
-    if (!attr) {
-        PTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    set_smem_attr(kern, smem);
     kern<<<1, NT, smem, p.stream>>>(static_cast<cplx<T>*>(z),
                                     p.has_probe ? p.probe.as<const cplx<T>>() : nullptr,
                                     p.pos.as<const int2>(), p.amp.as<const T>(), p.N, p.n, p.w,
@@ -796,11 +792,7 @@ void launch_pie_t(Plan& p, void* z, const void* wgt, double damping) {
 template <int M>
 void launch_pie_reg(Plan& p, void* z, const void* wgt, double damping) {
     constexpr size_t smem = pie_reg_smem_bytes<M>();
-    static bool attr = false;
-    if (!attr) {
-        PTG_CUDA(cudaFuncSetAttribute(k_pie_reg<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    set_smem_attr(k_pie_reg<M>, smem);
     k_pie_reg<M><<<1, M, smem, p.stream>>>(static_cast<float2*>(z), p.has_probe ? p.probe.as<const float2>() : nullptr,
                                           p.pos.as<const int2>(), p.amp.as<const float>(), p.N, p.n,
                                           static_cast<const float2*>(wgt), (float)damping);
@@ -999,7 +991,9 @@ void check_device(int device) {
 // (~100 us for a few MB): an MG/OPT cycle allocates ~30 vectors per level.
 // Keep the pool's memory reserved instead (bounded by the peak working set).
 static void keep_pool_memory(int device) {
+    static std::mutex mu;
     static bool done[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
     if (device < 0 || device >= 64 || done[device]) return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) {

@@ -13,8 +13,8 @@ namespace ptg {
 
 // PTG_LBFGS_DEBUG=1: host time inside the line-search synchronisations vs the
 // whole LBFGS call (dev instrumentation)
-static double g_sync_us = 0.0, g_graph_us = 0.0;
-static int g_graph_n = 0;
+static thread_local double g_sync_us = 0.0, g_graph_us = 0.0;   // one context per host thread
+static thread_local int g_graph_n = 0;
 static bool lbfgs_debug() {
     static const bool on = getenv("PTG_LBFGS_DEBUG") != nullptr;
     return on;
@@ -410,7 +410,7 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                     ctr.record(obj.level, obj.weight);   // charge before evaluating (solvers.hpp:33-36)
                     p.launches += G.launches;
                 }
-                static cudaEvent_t dbg_ev[2] = {nullptr, nullptr};
+                static thread_local cudaEvent_t dbg_ev[2] = {nullptr, nullptr};
                 if (lbfgs_debug()) {
                     if (!dbg_ev[0]) {
                         PTG_CUDA(cudaEventCreate(&dbg_ev[0]));
