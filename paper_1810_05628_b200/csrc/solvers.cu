@@ -15,6 +15,7 @@ namespace ptg {
 // whole LBFGS call (dev instrumentation)
 static thread_local double g_sync_us = 0.0, g_graph_us = 0.0;   // one context per host thread
 static thread_local int g_graph_n = 0;
+static thread_local double g_prep_us = 0.0;
 static bool lbfgs_debug() {
     static const bool on = getenv("PTG_LBFGS_DEBUG") != nullptr;
     return on;
@@ -149,6 +150,7 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     g_sync_us = 0.0;
     g_graph_us = 0.0;
     g_graph_n = 0;
+    g_prep_us = 0.0;
     int iters_done = 0;
     const size_t len = p.nn();
     DVec z(p, len), g(p, len), dir(p, len), nz(p, len), ng(p, len);
@@ -257,6 +259,7 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
         double* md_d = res_d + 9;
         if (lbfgs_debug()) { PTG_CUDA(cudaStreamSynchronize(p.stream)); dbg_mark("ws"); }
         for (int iter = 1; iter <= cfg.max_iters; ++iter) {
+            const auto t_iter = std::chrono::steady_clock::now();
             std::vector<const void*> sp, yp;
             std::vector<double> syv;
             for (int id : order) {
@@ -418,6 +421,8 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                     }
                     PTG_CUDA(cudaEventRecord(dbg_ev[0], p.stream));
                 }
+                if (lbfgs_debug())
+                    g_prep_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_iter).count();
                 PTG_CUDA(cudaGraphLaunch(G.exec, p.stream));
                 if (lbfgs_debug()) PTG_CUDA(cudaEventRecord(dbg_ev[1], p.stream));
                 const auto ts = std::chrono::steady_clock::now();
@@ -487,9 +492,10 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     PTG_CUDA(cudaStreamSynchronize(p.stream));
     if (lbfgs_debug() && iters_done > 0) {
         const double tot = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_call).count();
-        fprintf(stderr, "[lbfgs] n=%d iters %d: %.1f us/iter wall, %.1f us/iter in line-search syncs, graph %.1f us GPU |%s\n",
+        fprintf(stderr, "[lbfgs] n=%d iters %d: %.1f us/iter wall, %.1f us/iter in line-search syncs, graph %.1f us GPU, "
+                "host prep %.1f us |%s\n",
                 p.n, iters_done, tot / iters_done, g_sync_us / iters_done, g_graph_n ? g_graph_us / g_graph_n : 0.0,
-                dbg_log.c_str());
+                g_graph_n ? g_prep_us / g_graph_n : 0.0, dbg_log.c_str());
     }
     return out;
 }
