@@ -222,6 +222,52 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------- ours
+def transfer_rooflines(stream):
+    """restrictField / prolongField (n = 4096 complex64) and restrictData
+    (N = 3721, M = 256 float32): achieved GB/s over SURVEY 8(d)'s algorithmic
+    bytes (1.25 * 8 n^2, 1.25 * 8 n^2, 2 N (M/2)^2 4), 10 launches each."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1810_05628_b200 import _lib
+    lib = _lib.lib()
+    peaks, _ = load_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    n, N, M = 4096, 3721, 256
+    fine = torch.ones(n, n, dtype=torch.complex64, device="cuda")
+    coarse = torch.empty(n // 2, n // 2, dtype=torch.complex64, device="cuda")
+    dfine = torch.ones(N, M, M, dtype=torch.float32, device="cuda")
+    dcoarse = torch.empty(N, M // 2, M // 2, dtype=torch.float32, device="cuda")
+    st = C.c_void_p(stream.cuda_stream)
+    ops = {
+        "restrict_field": (lambda: lib.ptg_restrict_field_device(0, C.c_void_p(fine.data_ptr()), n,
+                                                                  C.c_void_p(coarse.data_ptr()), st),
+                           1.25 * 8 * n * n),
+        "prolong_field": (lambda: lib.ptg_prolong_field_device(0, C.c_void_p(coarse.data_ptr()), n // 2,
+                                                                C.c_void_p(fine.data_ptr()), st),
+                          1.25 * 8 * n * n),
+        "restrict_data": (lambda: lib.ptg_restrict_data_device(0, C.c_void_p(dfine.data_ptr()), N, M,
+                                                                C.c_void_p(dcoarse.data_ptr()), st),
+                          2.0 * N * (M // 2) ** 2 * 4),
+    }
+    out = {}
+    for name, (fn, nbytes) in ops.items():
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(10):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / 10 * 1e3
+        gbs = nbytes / (us * 1e-6) / 1e9
+        out[name] = {"us": us, "bytes": nbytes, "achieved_gbs": gbs, "frac_hbm": gbs / hbm}
+    return out
+
+
 def run_ours(args):
     import torch
     rank = int(os.environ.get("RANK", "0"))
@@ -451,6 +497,12 @@ def run_ours(args):
             plan3.close()
         except Exception as ex:   # noqa: BLE001
             extras["vcycle_error"] = str(ex)
+        # MG/OPT grid transfers (multigrid.cpp:34-77) at config 4's sizes, HBM
+        # rooflines with SURVEY 8(d)'s byte counts; inputs > L2, CUDA events
+        try:
+            extras["transfers"] = transfer_rooflines(stream)
+        except Exception as ex:   # noqa: BLE001
+            extras["transfers_error"] = str(ex)
         # CPU baseline on a bounded sample of the same workload
         try:
             host_data = plan.simulate(obj, copy_out=True)
