@@ -319,13 +319,16 @@ def run_ours(args):
     flush = torch.ones(128 << 20, dtype=torch.float32, device="cuda")
     flush_out = torch.empty(1, dtype=torch.float32, device="cuda")
 
+    halo = sharding.HaloExchange(cfg.n, overlap, cdt, "cuda") if (dist is not None and banded) else None
+
     def exchange(g, v):
         if dist is None:
             return
         if banded:
-            sharding.halo_exchange(g, overlap)   # shared band rows with the neighbours
-        else:
-            dist.all_reduce(torch.view_as_real(g))
+            # shared band rows + misfit: pack kernel, ONE all-gather, unpack kernel
+            halo(g, v)
+            return
+        dist.all_reduce(torch.view_as_real(g))
         dist.all_reduce(v[:1])
 
     def step():

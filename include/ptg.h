@@ -155,6 +155,21 @@ int ptg_restrict_field_device(int precision, const void *fine, int n, void *coar
 int ptg_prolong_field_device(int precision, const void *coarse, int nH, void *fine, void *stream);
 int ptg_restrict_data_device(int dtype, const void *fine, int N, int M, void *coarse, void *stream);
 
+/* ----------------------------------------------- multi-GPU band exchange */
+/* No reference counterpart (the reference is single-process): helpers of the
+ * band decomposition of SURVEY 8(e) (paper_1810_05628_b200/sharding.py).  A
+ * rank's n x n band shares `ov` gradient rows with each neighbour.  pack:
+ * [top ov rows][bottom ov rows][*val_dev (f64)] into `buf` (ptg_halo_bytes
+ * bytes); after an all-gather of every rank's buffer into `all` (world x
+ * ptg_halo_bytes), unpack adds the neighbours' rows to the band's own
+ * (own + received) and writes the rank-ordered sum of the misfits to *val_dev.
+ * Device pointers, plan precision; enqueued on `stream`. */
+size_t ptg_halo_bytes(int precision, int n, int ov);
+int ptg_halo_pack(int precision, const void *grad, int n, int ov, const double *val_dev, void *buf,
+                  void *stream);
+int ptg_halo_unpack(int precision, void *grad, int n, int ov, const void *all, int rank, int world,
+                    double *val_dev, void *stream);
+
 /* ------------------------------------------------------------- diagnostics */
 /* metrics.hpp:9-24 on the device: relativeError, magnitudeRelError and
  * phaseSSIM (11x11 Gaussian window, sigma 1.5, L = pi/2), fp64 arithmetic.

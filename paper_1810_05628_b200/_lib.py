@@ -107,6 +107,7 @@ EXPORTS = [
     "ptg_pie", "ptg_pie_sweep_device",
     "ptg_restrict_field", "ptg_prolong_field", "ptg_restrict_data",
     "ptg_restrict_field_device", "ptg_prolong_field_device", "ptg_restrict_data_device",
+    "ptg_halo_bytes", "ptg_halo_pack", "ptg_halo_unpack",
     "ptg_solver_cfg_default", "ptg_mg_cfg_default", "ptg_driver_cfg_default",
     "ptg_metrics_device", "ptg_metrics_host", "ptg_canonical_phase",
     "ptg_lbfgs", "ptg_truncated_newton", "ptg_hier_create", "ptg_hier_destroy", "ptg_hier_level",
@@ -150,6 +151,10 @@ def lib() -> C.CDLL:
     L.ptg_restrict_field_device.argtypes = [C.c_int, _vp, C.c_int, _vp, _vp]
     L.ptg_prolong_field_device.argtypes = [C.c_int, _vp, C.c_int, _vp, _vp]
     L.ptg_restrict_data_device.argtypes = [C.c_int, _vp, C.c_int, C.c_int, _vp, _vp]
+    L.ptg_halo_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
+    L.ptg_halo_bytes.restype = C.c_size_t
+    L.ptg_halo_pack.argtypes = [C.c_int, _vp, C.c_int, C.c_int, _vp, _vp, _vp]
+    L.ptg_halo_unpack.argtypes = [C.c_int, _vp, C.c_int, C.c_int, _vp, C.c_int, C.c_int, _vp, _vp]
     L.ptg_solver_cfg_default.argtypes = [C.POINTER(SolverCfg)]
     L.ptg_solver_cfg_default.restype = None
     L.ptg_mg_cfg_default.argtypes = [C.POINTER(MgCfg)]

@@ -369,6 +369,24 @@ int ptg_restrict_data_device(int dtype, const void* fine, int N, int M, void* co
     return guard([&] { ptg::dev_restrict_data(dtype, fine, N, M, coarse, 1.0 / 16.0, (cudaStream_t)stream); });
 }
 
+// ------------------------------------------------------ band exchange (halo.cu)
+size_t ptg_halo_bytes(int precision, int n, int ov) { return ptg::halo_bytes(precision, n, ov); }
+
+int ptg_halo_pack(int precision, const void* grad, int n, int ov, const double* val_dev, void* buf, void* stream) {
+    return guard([&] {
+        if (!grad || !val_dev || !buf) ptg::raise(PTG_ERR_CONFIG, "ptg_halo_pack: null pointer");
+        ptg::dev_halo_pack(precision, grad, n, ov, val_dev, buf, (cudaStream_t)stream);
+    });
+}
+
+int ptg_halo_unpack(int precision, void* grad, int n, int ov, const void* all, int rank, int world, double* val_dev,
+                    void* stream) {
+    return guard([&] {
+        if (!grad || !val_dev || !all) ptg::raise(PTG_ERR_CONFIG, "ptg_halo_unpack: null pointer");
+        ptg::dev_halo_unpack(precision, grad, n, ov, all, rank, world, val_dev, (cudaStream_t)stream);
+    });
+}
+
 // ---------------------------------------------------------------- solvers
 int ptg_lbfgs(ptg_plan* plan, int metric, const double* v, const double* z0,
               const ptg_solver_cfg* cfg, double* z_out, double* grad_out, ptg_report* rep,

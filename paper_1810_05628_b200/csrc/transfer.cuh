@@ -11,4 +11,10 @@ void dev_prolong_field(int prec, const void* coarse, int nH, void* fine, cudaStr
 void dev_restrict_data(int dtype, const void* fine, int N, int M, void* coarse, double scale,
                        cudaStream_t s);
 
+// band-decomposition exchange (halo.cu)
+size_t halo_bytes(int prec, int n, int ov);
+void dev_halo_pack(int prec, const void* g, int n, int ov, const double* val, void* buf, cudaStream_t s);
+void dev_halo_unpack(int prec, void* g, int n, int ov, const void* all, int rank, int world, double* val,
+                     cudaStream_t s);
+
 }  // namespace ptg

@@ -304,3 +304,41 @@ def test_graph_replayed_host_eval(with_shift):
         val_d = plan.evaluate_device(zt, gt, v=vt)
         assert val_h == val_d, call
         assert np.array_equal(gp.numpy(), gt.cpu().numpy().astype(np.complex128)), call
+
+
+@pytest.mark.parametrize("precision", ["c64", "c128"])
+def test_halo_exchange_kernels(precision):
+    """csrc/halo.cu (band exchange): pack every simulated rank's band, concatenate
+    the buffers as the all-gather would, unpack on each rank: neighbours' rows
+    added to the own rows (bitwise own + received), misfits summed in rank order."""
+    import torch
+    from paper_1810_05628_b200 import _lib, sharding
+    lib = _lib.lib()
+    world, n, ov = 3, 64, 16
+    cdt = torch.complex64 if precision == "c64" else torch.complex128
+    prec = 0 if precision == "c64" else 1
+    nb = int(lib.ptg_halo_bytes(prec, n, ov))
+    assert nb == sharding.halo_bytes(n, ov, 8 if precision == "c64" else 16)
+    rng = np.random.default_rng(5)
+    grads = [torch.from_numpy((rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))).astype(
+        np.complex64 if precision == "c64" else np.complex128)).cuda() for _ in range(world)]
+    vals = [torch.tensor([float(r) + 0.25, 0.0], dtype=torch.float64, device="cuda") for r in range(world)]
+    bufs = []
+    for r in range(world):
+        b = torch.zeros(nb, dtype=torch.uint8, device="cuda")
+        assert lib.ptg_halo_pack(prec, grads[r].data_ptr(), n, ov, vals[r].data_ptr(), b.data_ptr(), None) == 0
+        bufs.append(b)
+    allb = torch.cat(bufs)
+    torch.cuda.synchronize()
+    for r in range(world):
+        g = grads[r].clone()
+        v = vals[r].clone()
+        assert lib.ptg_halo_unpack(prec, g.data_ptr(), n, ov, allb.data_ptr(), r, world, v.data_ptr(), None) == 0
+        torch.cuda.synchronize()
+        want = grads[r].cpu().numpy().copy()
+        if r > 0:
+            want[:ov] = want[:ov] + grads[r - 1].cpu().numpy()[n - ov:]
+        if r + 1 < world:
+            want[n - ov:] = want[n - ov:] + grads[r + 1].cpu().numpy()[:ov]
+        assert np.array_equal(g.cpu().numpy(), want)
+        assert float(v[0].cpu()) == sum(float(k) + 0.25 for k in range(world))

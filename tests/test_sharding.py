@@ -118,3 +118,64 @@ def test_band_decomposition_matches_global_object(world):
         rank, val, full_val, grad_rel = q.get(timeout=5)
         assert abs(val - full_val) <= 1e-12 * abs(full_val)
         assert grad_rel <= 1e-12
+
+
+def _fused_band_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import ptgo
+        from paper_1810_05628_b200 import sharding, synth
+        nb, M, s = 40, 16, 8
+        ov = M - s
+        H = world * (nb - ov) + ov
+        obj = synth.make_object(H, 2.0)
+        probe = synth.make_probe(M, 4.0, 0.01)
+        loc = np.array([[r, c] for r in range(0, nb - M + 1, s) for c in range(0, nb - M + 1, s)], np.int32)
+        glob = np.concatenate([loc + [sharding.band_offset(b, nb, ov), 0] for b in range(world)])
+        data = ptgo.simulate(H, M, M, glob, obj, probe)
+        z = obj * 0.9 + 0.05
+        off = sharding.band_offset(rank, nb, ov)
+        k = loc.shape[0]
+        band = np.ascontiguousarray(z[off:off + nb, :nb])
+        val, g = ptgo.evaluate(ptgo.Problem(nb, M, M, loc, data[rank * k:(rank + 1) * k], probe), band)
+        gt = torch.from_numpy(g.copy())
+        vt = torch.tensor([val, 0.0], dtype=torch.float64)
+        ex = sharding.HaloExchange(nb, ov, gt.dtype, "cpu")
+        ex(gt, vt)
+        full_val, full_g = ptgo.evaluate(ptgo.Problem(H, M, M, glob, data, probe), z)
+        want = full_g[off:off + nb, :nb]
+        # the rows shared with a neighbour must be bitwise equal on both ranks
+        shared = [gt[:ov].numpy().copy(), gt[nb - ov:].numpy().copy()]
+        q.put((rank, float(vt[0]), full_val, float(np.linalg.norm(gt.numpy() - want) / np.linalg.norm(want)),
+               shared))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_halo_exchange_matches_global_object(world):
+    """The band exchange as one all-gather (sharding.HaloExchange, the layout of
+    csrc/halo.cu): the exchanged gradients equal the global gradient's rows, the
+    misfit is the global misfit, and shared rows are bitwise equal on both sides."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_fused_band_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(150)
+    assert all(p.exitcode == 0 for p in ps)
+    got = {}
+    for _ in range(world):
+        rank, val, full_val, grad_rel, shared = q.get(timeout=5)
+        assert abs(val - full_val) <= 1e-12 * abs(full_val)
+        assert grad_rel <= 1e-12
+        got[rank] = shared
+    for r in range(world - 1):
+        assert np.array_equal(got[r][1], got[r + 1][0])
