@@ -75,7 +75,7 @@ struct Plan {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     // banded host evaluation (plan_eval_host): copy-in / copy-out streams + events
-    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaStream_t s_in = nullptr, s_out = nullptr, s_in2 = nullptr, s_out2 = nullptr;
     // solver graphs: side stream + fork/join events (d_lbfgs products)
     cudaStream_t s_side = nullptr;
     cudaEvent_t ev_side[2] = {nullptr, nullptr};
