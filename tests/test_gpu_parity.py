@@ -342,3 +342,37 @@ def test_halo_exchange_kernels(precision):
             want[n - ov:] = want[n - ov:] + grads[r + 1].cpu().numpy()[:ov]
         assert np.array_equal(g.cpu().numpy(), want)
         assert float(v[0].cpu()) == sum(float(k) + 0.25 for k in range(world))
+
+
+def test_transfer_device_kernels_c64_f32():
+    """The float4-vectorised complex64 / float32 transfer kernels (transfer.cu)
+    against the reference's arithmetic in the same precision and order
+    (multigrid.cpp:34-77): bit-exact."""
+    import torch
+    from paper_1810_05628_b200 import _lib
+    lib = _lib.lib()
+    rng = np.random.default_rng(9)
+    n = 96
+    f = (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))).astype(np.complex64)
+    ft = torch.from_numpy(f).cuda()
+    ct = torch.empty(n // 2, n // 2, dtype=torch.complex64, device="cuda")
+    assert lib.ptg_restrict_field_device(0, ft.data_ptr(), n, ct.data_ptr(), None) == 0
+    a, b, c, d = f[0::2, 0::2], f[0::2, 1::2], f[1::2, 0::2], f[1::2, 1::2]
+    want = ((a + b) + (c + d)) * np.float32(0.25)
+    torch.cuda.synchronize()
+    assert np.array_equal(ct.cpu().numpy(), want)
+    pt = torch.empty(n, n, dtype=torch.complex64, device="cuda")
+    assert lib.ptg_prolong_field_device(0, ct.data_ptr(), n // 2, pt.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(pt.cpu().numpy(), np.repeat(np.repeat(want, 2, 0), 2, 1))
+    for M in (16, 32, 64):   # float4 path (M % 16 == 0)
+        N = 5
+        dd = rng.random((N, M, M)).astype(np.float32)
+        dt = torch.from_numpy(dd).cuda()
+        ot = torch.empty(N, M // 2, M // 2, dtype=torch.float32, device="cuda")
+        assert lib.ptg_restrict_data_device(0, dt.data_ptr(), N, M, ot.data_ptr(), None) == 0
+        MH = M // 2
+        idx = (((np.arange(MH) + MH // 2) % MH) + 3 * M // 4) % M
+        want_d = dd[:, idx][:, :, idx] * np.float32(1.0 / 16.0)
+        torch.cuda.synchronize()
+        assert np.array_equal(ot.cpu().numpy(), want_d), M
