@@ -20,6 +20,11 @@
 //   * the probe products (P o x before, conj(P) o r after) run as cooperative
 //     shared-memory passes when no line is live in registers, so the probe
 //     loads (L2-resident) are deep in flight without register pressure.
+//
+// Timing-only build variants (tools/build_variant.sh, never the shipped
+// library): ABL_NOPREF / ABL_NOSPEC / ABL_NOTRANS / ABL_NOSTORE remove one
+// phase each (results invalid), ABL_TIMELINE records per-CTA %globaltimer
+// stamps (tools/timeline.py).  profiles/r01_frame_analysis.txt has the numbers.
 #pragma once
 
 #include <cuda.h>
