@@ -427,9 +427,16 @@ def run_ours(args):
     h2d = zh.nbytes
     d2h = gh.nbytes + 8
     # warm-up: the first call with these buffers runs eagerly, the second
-    # captures the replay graph; a few more settle clocks and caches
-    for _ in range(10):
-        plan.evaluate(zh, out=gh) if world == 1 else None
+    # captures the replay graph; then ~0.4 s of calls: a fresh process's
+    # per-call time falls from ~350 to ~210 us over its first ~500 calls
+    # (tools/e2e_warmup_probe.py) as the mostly idle GPU / link ramps up --
+    # the steady state is what a solver calling ptg_eval in a loop sees
+    if world == 1:
+        t_w = time.perf_counter()
+        nw = 0
+        while nw < 10 or time.perf_counter() - t_w < 0.4:
+            plan.evaluate(zh, out=gh)
+            nw += 1
     e2e_steps = max(args.steps, 100)
     if world == 1:
         torch.cuda.synchronize()
