@@ -258,10 +258,16 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
         double* stats_d = res_d + 1;
         double* md_d = res_d + 9;
         if (lbfgs_debug()) { PTG_CUDA(cudaStreamSynchronize(p.stream)); dbg_mark("ws"); }
+        // per-iteration host scratch, reused (no allocations on the iteration path)
+        std::vector<const void*> sp, yp, msp, myp;
+        std::vector<double> syv, t, u, c, rhs;
+        for (auto* vec : {&sp, &yp, &msp, &myp}) vec->reserve(mem + 2);
+        for (auto* vec : {&syv, &t, &u, &c, &rhs}) vec->reserve(mem + 2);
         for (int iter = 1; iter <= cfg.max_iters; ++iter) {
             const auto t_iter = std::chrono::steady_clock::now();
-            std::vector<const void*> sp, yp;
-            std::vector<double> syv;
+            sp.clear();
+            yp.clear();
+            syv.clear();
             for (int id : order) {
                 sp.push_back(slots[id].s.p);
                 yp.push_back(slots[id].y.p);
@@ -283,7 +289,10 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
                     auto sy = [&](int i, int j) { return SY[(size_t)order[i] * nslot_max + order[j]]; };
                     auto yy = [&](int i, int j) { return YY[(size_t)order[i] * nslot_max + order[j]]; };
                     const double gamma = sy(k - 1, k - 1) / yy(k - 1, k - 1);
-                    std::vector<double> t(k), u(k), c(k), rhs(k);
+                    t.assign(k, 0.0);
+                    u.assign(k, 0.0);
+                    c.assign(k, 0.0);
+                    rhs.assign(k, 0.0);
                     for (int i = k - 1; i >= 0; --i) {   // R t = S'g (R upper triangular)
                         double a = Sg[order[i]];
                         for (int j = i + 1; j < k; ++j) a -= sy(i, j) * t[j];
@@ -327,7 +336,8 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
             // pair statistics (+ isFinite of the new iterate) of the accepted point
             // and, in compact mode, every product the next direction needs,
             // enqueued speculatively behind the first trial's evaluation
-            std::vector<const void*> msp(sp), myp(yp);
+            msp.assign(sp.begin(), sp.end());
+            myp.assign(yp.begin(), yp.end());
             msp.push_back(pr.s.p);
             myp.push_back(pr.y.p);
             if (compact) {
