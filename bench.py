@@ -445,16 +445,29 @@ def run_ours(args):
             plan.evaluate(zh, out=gh)
         e2e_s = time.perf_counter() - t0
     else:
+        # per rank: pinned complex128 band in (H2D), device conversion, the
+        # evaluation and the band exchange, conversion back, pinned complex128
+        # gradient out (D2H) and the value read -- the host API's data path
         zt = torch.empty_like(z)
+        z128 = torch.empty(cfg.n, cfg.n, dtype=torch.complex128, device="cuda")
+        g128 = torch.empty_like(z128)
+        zh_t, gh_t = torch.from_numpy(zh), torch.from_numpy(gh)
+
+        def e2e_step():
+            z128.copy_(zh_t, non_blocking=True)
+            zt.copy_(z128)
+            plan.evaluate_device(zt, grad, value_dev=val, sync_value=False)
+            exchange(grad, val)
+            g128.copy_(grad)
+            gh_t.copy_(g128, non_blocking=True)
+            float(val[0].item())
+        for _ in range(300):   # a fixed count on every rank (collectives inside)
+            e2e_step()
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            zt.copy_(torch.from_numpy(zh).to(cdt), non_blocking=False)
-            plan.evaluate_device(zt, grad, value_dev=val, sync_value=False)
-            exchange(grad, val)
-            torch.from_numpy(gh).copy_(grad.to(torch.complex128))
-            float(val[0].item())
+            e2e_step()
         e2e_s = time.perf_counter() - t0
         tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
