@@ -106,7 +106,15 @@ class ClockSampler:
             import pynvml
             pynvml.nvmlInit()
             self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            # NVML numbers GPUs physically; CUDA_VISIBLE_DEVICES renumbers them
+            # for CUDA -- look the device up by its PCI bus id
+            try:
+                import torch
+                pr = torch.cuda.get_device_properties(index)
+                bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+                self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
             self.nv = None
@@ -396,8 +404,7 @@ def run_ours(args):
         return sum(s.elapsed_time(e) for s, e in zip(starts, ends))
 
     # headline: the production launch sequence (PDL-chained kernels, no probes)
-    sampler = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ
-                           else local)
+    sampler = ClockSampler(torch.cuda.current_device())
     l0 = plan.launch_count
     sampler.start()
     t_ms = timed_loop()

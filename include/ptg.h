@@ -99,6 +99,9 @@ int ptg_plan_set_data_device(ptg_plan *plan, const void *dev_data, int dtype);
  * overlapping H2D copy + on-device conversion).  Errors: 2 (Io) for
  * open/magic/truncation, 11 (Geometry) if the stack is not N patterns of side M. */
 int ptg_plan_load_ptyf(ptg_plan *plan, const char *path);
+/* the resident data back to the host as N*M*M float64: the intensities d
+ * (metric PTG_INTENSITY) or the amplitudes sqrt(d) (PTG_DISTANCE) */
+int ptg_plan_get_data(ptg_plan *plan, int metric, double *out);
 /* bytes of HBM the plan holds, and its dims (any pointer may be NULL) */
 int ptg_plan_info(const ptg_plan *plan, int *n, int *M, int *w, int *N, int *precision,
                   size_t *device_bytes);
@@ -131,6 +134,27 @@ int ptg_project_modulus(ptg_plan *plan, const double *z, int k, double *frame);
  * the plan's resident data (and optionally a host copy, N*M*M doubles). */
 int ptg_simulate(ptg_plan *plan, const double *z, double *data_out);
 int ptg_simulate_device(ptg_plan *plan, const void *z);
+
+/* ---------------------------------------------------------------- noise */
+/* addNoise (forward.hpp:44-48, forward.cpp:56-86) in place on the plan's
+ * resident intensities (the amplitudes are rebuilt): per pattern
+ * eps = level ||d|| / ||g|| g with g_i = sqrt(-2 log(1-u1)) cos(2 pi u2)
+ * (rng::gaussian, rng.hpp:18-24), d <- max(d + eps, 0).  uniforms = NULL
+ * draws (u1, u2) of pixel i of pattern j from Philox4x64-10 with counter
+ * (i, j, 1, 0) and key (seed, 0); otherwise `uniforms` is a host array of
+ * 2 N M^2 doubles in the reference's draw order (pattern, pixel, u1/u2), so
+ * the result follows the reference's std::mt19937_64 stream exactly.
+ * DomainError for level < 0 (forward.cpp:57). */
+int ptg_add_noise(ptg_plan *plan, double level, uint64_t seed, const double *uniforms);
+/* Poisson photon noise at `photons` per pattern (BASELINE configs 4/5; no
+ * reference counterpart): lambda = d photons / sum(d), d <- k / scale with
+ * k ~ Poisson(lambda) (inversion below 10, PTRS transformed rejection above),
+ * uniforms from Philox4x64-10 with counter (pixel, pattern, 2, block). */
+int ptg_add_poisson(ptg_plan *plan, double photons, uint64_t seed);
+/* raw Philox4x64-10 output on `device`: out[4 b + k] = word k of
+ * philox(counter (ctr[0] + b, ctr[1], ctr[2], ctr[3]), key), b < nblocks
+ * (host out; for pinning the generator against numpy.random.Philox) */
+int ptg_philox4x64(int device, const uint64_t ctr[4], const uint64_t key[2], size_t nblocks, uint64_t *out);
 
 /* ----------------------------------------------------------------- PIE */
 typedef struct { double weighted, value, gnorm; } ptg_hist;

@@ -1157,3 +1157,119 @@ done:
     free(z); free(g); free(nz); free(ng); free(vzero);
     return rc;
 }
+
+/* ------------------------------------------------------------------ noise */
+/* Philox4x64-10 (Salmon et al., SC'11; the bit generator of
+ * numpy.random.Philox): counter c, key k -> 4 x 64-bit words. */
+void ptgo_philox4x64(const uint64_t ctr[4], const uint64_t key[2], uint64_t out[4]) {
+    const uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+    const uint64_t W0 = 0x9E3779B97F4A7C15ull, W1 = 0xBB67AE8584CAA73Bull;
+    uint64_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3], k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; ++r) {
+        const unsigned __int128 p0 = (unsigned __int128)M0 * c0, p1 = (unsigned __int128)M1 * c2;
+        const uint64_t hi0 = (uint64_t)(p0 >> 64), lo0 = (uint64_t)p0;
+        const uint64_t hi1 = (uint64_t)(p1 >> 64), lo1 = (uint64_t)p1;
+        c0 = hi1 ^ c1 ^ k0;
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ k1;
+        c3 = lo0;
+        k0 += W0;
+        k1 += W1;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+static double u01(uint64_t x) { return (double)(x >> 11) * 0x1.0p-53; }   /* rng.hpp:14-16 */
+
+static double gauss_at(size_t i, int j, uint64_t seed, const double *uni, size_t mm) {
+    double u1, u2;
+    if (uni) {
+        u1 = uni[2 * ((size_t)j * mm + i)];
+        u2 = uni[2 * ((size_t)j * mm + i) + 1];
+    } else {
+        const uint64_t c[4] = {(uint64_t)i, (uint64_t)j, 1, 0}, k[2] = {seed, 0};
+        uint64_t r[4];
+        ptgo_philox4x64(c, k, r);
+        u1 = u01(r[0]);
+        u2 = u01(r[1]);
+    }
+    const double rr = sqrt(-2.0 * log(1.0 - u1));   /* rng::gaussian, rng.hpp:18-24 */
+    return rr * cos(6.283185307179586476925286766559 * u2);
+}
+
+/* addNoise (forward.cpp:56-86): per pattern eps = level ||d|| / ||g|| g,
+ * out = max(d + eps, 0).  uni = NULL: Philox uniforms (the GPU's stream);
+ * otherwise 2 N mm uniforms in the reference's draw order. */
+int ptgo_add_noise(int N, size_t mm, const double *d, double level, uint64_t seed, const double *uni,
+                   double *out) {
+    if (level < 0.0) return fail(PTGO_DOMAIN, "noise level must be non-negative");
+    for (int j = 0; j < N; ++j) {
+        const double *dj = d + (size_t)j * mm;
+        double dsq = 0.0, gsq = 0.0;
+        for (size_t i = 0; i < mm; ++i) {
+            const double g = gauss_at(i, j, seed, uni, mm);
+            dsq += dj[i] * dj[i];
+            gsq += g * g;
+        }
+        const double scale = gsq > 0.0 ? level * sqrt(dsq) / sqrt(gsq) : 0.0;
+        for (size_t i = 0; i < mm; ++i) {
+            const double v = dj[i] + gauss_at(i, j, seed, uni, mm) * scale;
+            out[(size_t)j * mm + i] = v > 0.0 ? v : 0.0;
+        }
+    }
+    return PTGO_OK;
+}
+
+typedef struct { uint64_t i, j, seed, b; uint64_t r[4]; int k; } ustream;
+static double us_next(ustream *s) {
+    if (s->k == 4) {
+        const uint64_t c[4] = {s->i, s->j, 2, s->b++}, key[2] = {s->seed, 0};
+        ptgo_philox4x64(c, key, s->r);
+        s->k = 0;
+    }
+    return u01(s->r[s->k++]);
+}
+
+/* Poisson(lam): inversion below 10, Hormann's PTRS above (the GPU's sampler) */
+static double poisson_sample(double lam, ustream *us) {
+    if (!(lam > 0.0)) return 0.0;
+    if (lam < 10.0) {
+        const double u = us_next(us);
+        double p = exp(-lam), F = p;
+        int k = 0;
+        while (u > F && k < 1000) { ++k; p *= lam / k; F += p; }
+        return (double)k;
+    }
+    const double slam = sqrt(lam), loglam = log(lam);
+    const double b = 0.931 + 2.53 * slam, a = -0.059 + 0.02483 * b;
+    const double invalpha = 1.1239 + 1.1328 / (b - 3.4), vr = 0.9277 - 3.6224 / (b - 2.0);
+    for (int it = 0; it < 10000; ++it) {
+        const double U = us_next(us) - 0.5, V = us_next(us);
+        const double usv = 0.5 - fabs(U);
+        const double k = floor((2.0 * a / usv + b) * U + lam + 0.43);
+        if (usv >= 0.07 && V <= vr) return k;
+        if (k < 0.0 || (usv < 0.013 && V > usv)) continue;
+        if (log(V) + log(invalpha) - log(a / (usv * usv) + b) <= -lam + k * loglam - lgamma(k + 1.0)) return k;
+    }
+    return floor(lam);
+}
+
+/* Poisson photon noise at `photons` per pattern: out = k / scale */
+int ptgo_add_poisson(int N, size_t mm, const double *d, double photons, uint64_t seed, double *out) {
+    if (!(photons > 0.0)) return fail(PTGO_DOMAIN, "photon budget must be positive");
+    for (int j = 0; j < N; ++j) {
+        const double *dj = d + (size_t)j * mm;
+        double tot = 0.0;
+        for (size_t i = 0; i < mm; ++i) tot += dj[i];
+        const double scale = tot > 0.0 ? photons / tot : 0.0;
+        for (size_t i = 0; i < mm; ++i) {
+            double v = 0.0;
+            if (scale > 0.0) {
+                ustream us = {(uint64_t)i, (uint64_t)j, seed, 0, {0, 0, 0, 0}, 4};
+                v = poisson_sample(dj[i] * scale, &us) / scale;
+            }
+            out[(size_t)j * mm + i] = v;
+        }
+    }
+    return PTGO_OK;
+}

@@ -168,6 +168,12 @@ int ptgo_mgopt_driver(const ptgo_hierarchy *h, const double *z0,
                       const ptgo_driver_cfg *cfg, ptgo_counter *ctr, double *z_out,
                       double *value_out, double *grad_out, ptgo_report *rep);
 
+/* noise (forward.cpp:56-86) and the GPU's counter-based generator / Poisson sampler */
+void ptgo_philox4x64(const uint64_t ctr[4], const uint64_t key[2], uint64_t out[4]);
+int ptgo_add_noise(int N, size_t mm, const double *d, double level, uint64_t seed, const double *uni,
+                   double *out);
+int ptgo_add_poisson(int N, size_t mm, const double *d, double photons, uint64_t seed, double *out);
+
 #ifdef __cplusplus
 }
 #endif

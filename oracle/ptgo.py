@@ -231,6 +231,53 @@ def simulate(n: int, M: int, w: int, pos, z, probe=None) -> np.ndarray:
     return out
 
 
+def philox4x64(ctr, key) -> np.ndarray:
+    """One Philox4x64-10 block (4 uint64 words)."""
+    c = np.ascontiguousarray(ctr, dtype=np.uint64)
+    k = np.ascontiguousarray(key, dtype=np.uint64)
+    out = np.zeros(4, np.uint64)
+    u64p = C.POINTER(C.c_uint64)
+    lib().ptgo_philox4x64(c.ctypes.data_as(u64p), k.ctypes.data_as(u64p), out.ctypes.data_as(u64p))
+    return out
+
+
+def add_noise(d, level: float, seed: int = 0, uniforms=None) -> np.ndarray:
+    """addNoise (forward.cpp:56-86) on a stack d [N, m, m]; uniforms None = Philox stream."""
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    N, mm = d.shape[0], int(np.prod(d.shape[1:]))
+    out = np.empty_like(d)
+    u = None if uniforms is None else np.ascontiguousarray(uniforms, dtype=np.float64)
+    _check(lib().ptgo_add_noise(C.c_int(N), C.c_size_t(mm), _ptr(d), C.c_double(level), C.c_uint64(seed),
+                                _ptr(u) if u is not None else None, _ptr(out)))
+    return out
+
+
+def add_poisson(d, photons: float, seed: int = 4) -> np.ndarray:
+    """Poisson photon noise, the GPU's sampler restated (Philox uniforms)."""
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    N, mm = d.shape[0], int(np.prod(d.shape[1:]))
+    out = np.empty_like(d)
+    _check(lib().ptgo_add_poisson(C.c_int(N), C.c_size_t(mm), _ptr(d), C.c_double(photons), C.c_uint64(seed),
+                                  _ptr(out)))
+    return out
+
+
+def ref_add_noise(d, level: float, seed: int) -> np.ndarray:
+    """The reference's own addNoise (std::mt19937_64 stream)."""
+    d = np.ascontiguousarray(d, dtype=np.float64)
+    out = np.empty_like(d)
+    _check_ref(ref().ptref_add_noise(C.c_int(d.shape[0]), C.c_int(d.shape[1]), _ptr(d), C.c_double(level),
+                                     C.c_uint64(seed), _ptr(out)))
+    return out
+
+
+def ref_uniform_stream(seed: int, count: int) -> np.ndarray:
+    """The first `count` rng::uniform01 draws of std::mt19937_64(seed) (rng.hpp:14-16)."""
+    out = np.empty(count, np.float64)
+    _check_ref(ref().ptref_uniform_stream(C.c_uint64(seed), C.c_size_t(count), _ptr(out)))
+    return out
+
+
 def restrict_field(f) -> np.ndarray:
     f = _c128(f)
     out = np.zeros((f.shape[0] // 2, f.shape[0] // 2), np.complex128)

@@ -329,3 +329,33 @@ int ptref_canonical_phase(int n, const double* z, double* out) {
 }
 
 }  // extern "C"
+
+// ---- noise (forward.cpp:56-86, rng.hpp:14-24), for pinning ptg_add_noise
+extern "C" {
+// addNoise on N patterns of side m (RealGrid m x m): out = the reference's
+// max(d + eps, 0) with a std::mt19937_64 engine seeded by `seed`
+int ptref_add_noise(int N, int m, const double* data, double level, uint64_t seed, double* out) {
+    return guard([&] {
+        DiffractionStack d;
+        d.n = m;
+        const std::size_t mm = static_cast<std::size_t>(m) * m;
+        for (int k = 0; k < N; ++k) {
+            RealGrid g(m);
+            std::memcpy(g.data(), data + k * mm, sizeof(double) * mm);
+            d.patterns.push_back(std::move(g));
+        }
+        NoiseSpec spec;
+        spec.level = level;
+        spec.seed = seed;
+        DiffractionStack o = addNoise(d, spec);
+        for (int k = 0; k < N; ++k) std::memcpy(out + k * mm, o.patterns[k].data(), sizeof(double) * mm);
+    });
+}
+// the first `count` rng::uniform01 draws of std::mt19937_64(seed)
+int ptref_uniform_stream(uint64_t seed, std::size_t count, double* out) {
+    return guard([&] {
+        rng::Engine eng(seed);
+        for (std::size_t i = 0; i < count; ++i) out[i] = rng::uniform01(eng);
+    });
+}
+}

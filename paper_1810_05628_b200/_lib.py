@@ -101,9 +101,10 @@ class Report(C.Structure):
 EXPORTS = [
     "ptg_last_error", "ptg_version", "ptg_device_count",
     "ptg_plan_create", "ptg_plan_destroy", "ptg_plan_set_stream", "ptg_plan_set_data",
-    "ptg_plan_set_data_device", "ptg_plan_load_ptyf", "ptg_plan_info", "ptg_plan_launch_count",
+    "ptg_plan_set_data_device", "ptg_plan_load_ptyf", "ptg_plan_get_data", "ptg_plan_info", "ptg_plan_launch_count",
     "ptg_plan_set_timing", "ptg_plan_get_timing",
     "ptg_eval", "ptg_eval_device", "ptg_project_modulus", "ptg_simulate", "ptg_simulate_device",
+    "ptg_add_noise", "ptg_add_poisson", "ptg_philox4x64",
     "ptg_pie", "ptg_pie_sweep_device",
     "ptg_restrict_field", "ptg_prolong_field", "ptg_restrict_data",
     "ptg_restrict_field_device", "ptg_prolong_field_device", "ptg_restrict_data_device",
@@ -132,6 +133,7 @@ def lib() -> C.CDLL:
     L.ptg_plan_set_data.argtypes = [_vp, _vp, C.c_int]
     L.ptg_plan_set_data_device.argtypes = [_vp, _vp, C.c_int]
     L.ptg_plan_load_ptyf.argtypes = [_vp, C.c_char_p]
+    L.ptg_plan_get_data.argtypes = [_vp, C.c_int, _vp]
     L.ptg_metrics_device.argtypes = [C.c_int, _vp, _vp, C.c_int, C.c_uint, C.POINTER(Metrics), _vp]
     L.ptg_metrics_host.argtypes = [_vp, _vp, C.c_int, C.c_uint, C.POINTER(Metrics)]
     L.ptg_canonical_phase.argtypes = [_vp, C.c_int, _vp]
@@ -145,6 +147,9 @@ def lib() -> C.CDLL:
     L.ptg_pie.argtypes = [_vp, _vp, C.c_double, C.c_int, C.c_double, _dp, C.POINTER(Hist), C.c_int,
                           C.POINTER(C.c_int), _dp, C.POINTER(C.c_int)]
     L.ptg_pie_sweep_device.argtypes = [_vp, _vp, C.c_double]
+    L.ptg_add_noise.argtypes = [_vp, C.c_double, C.c_uint64, _vp]
+    L.ptg_add_poisson.argtypes = [_vp, C.c_double, C.c_uint64]
+    L.ptg_philox4x64.argtypes = [C.c_int, _vp, _vp, C.c_size_t, _vp]
     L.ptg_restrict_field.argtypes = [_vp, C.c_int, _vp]
     L.ptg_prolong_field.argtypes = [_vp, C.c_int, _vp]
     L.ptg_restrict_data.argtypes = [_vp, C.c_int, C.c_int, _vp]

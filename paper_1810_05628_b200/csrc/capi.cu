@@ -174,6 +174,22 @@ int ptg_plan_load_ptyf(ptg_plan* plan, const char* path) {
     return guard([&] { ptg::plan_load_ptyf(P(plan), path); });
 }
 
+int ptg_plan_get_data(ptg_plan* plan, int metric, double* out) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        ptg::LaunchScope ls(p);
+        ptg::plan_ensure(p, metric);
+        const size_t len = (size_t)p.N * p.MM();
+        if (!len) return;
+        ptg::DevMem d64;
+        d64.alloc(len * 8);
+        const void* src = metric == PTG_DISTANCE ? p.amp.p : p.inten.p;
+        ptg::dev_real_convert(PTG_C128, d64.p, p.prec == PTG_C64 ? PTG_F32 : PTG_F64, src, len, p.stream);
+        PTG_CUDA(cudaMemcpyAsync(out, d64.p, len * 8, cudaMemcpyDeviceToHost, p.stream));
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+    });
+}
+
 int ptg_plan_info(const ptg_plan* plan, int* n, int* M, int* w, int* N, int* precision,
                   size_t* device_bytes) {
     return guard([&] {
@@ -276,6 +292,30 @@ int ptg_simulate(ptg_plan* plan, const double* z, double* data_out) {
 
 int ptg_simulate_device(ptg_plan* plan, const void* z) {
     return guard([&] { ptg::plan_simulate(P(plan), z); });
+}
+
+int ptg_add_noise(ptg_plan* plan, double level, uint64_t seed, const double* uniforms) {
+    return guard([&] { ptg::plan_add_noise(P(plan), level, (unsigned long long)seed, uniforms); });
+}
+
+int ptg_add_poisson(ptg_plan* plan, double photons, uint64_t seed) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        ptg::plan_add_poisson(p, photons, (unsigned long long)seed);
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+    });
+}
+
+int ptg_philox4x64(int device, const uint64_t ctr[4], const uint64_t key[2], size_t nblocks, uint64_t* out) {
+    return guard([&] {
+        ptg::check_device_public(device);
+        ptg::DevMem d;
+        d.alloc(std::max<size_t>(1, nblocks) * 32);
+        const unsigned long long c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]}, k[2] = {key[0], key[1]};
+        ptg::dev_philox_raw(d.as<unsigned long long>(), nblocks, c, k, nullptr);
+        PTG_CUDA(cudaDeviceSynchronize());
+        if (nblocks) PTG_CUDA(cudaMemcpy(out, d.p, nblocks * 32, cudaMemcpyDeviceToHost));
+    });
 }
 
 int ptg_pie(ptg_plan* plan, double* z, double gamma, int sweeps, double max_weighted,

@@ -66,7 +66,8 @@ size_t halo_bytes(int prec, int n, int ov) {
 }
 
 void dev_halo_pack(int prec, const void* g, int n, int ov, const double* val, void* buf, cudaStream_t s) {
-    if (n < 1 || ov < 0 || ov > n) raise(PTG_ERR_GEOMETRY, "halo: need 0 <= overlap <= n");
+    if (n < 1 || ov < 0 || 2 * (size_t)ov > (size_t)n)   // top and bottom halo rows must not overlap
+        raise(PTG_ERR_GEOMETRY, "halo: need 0 <= 2 * overlap <= n");
     const size_t m = (size_t)ov * n;
     if (prec == PTG_C64)
         k_halo_pack<float><<<halo_grid(m), 256, 0, s>>>((const float2*)g, n, ov, val, (unsigned char*)buf);
@@ -78,7 +79,8 @@ void dev_halo_pack(int prec, const void* g, int n, int ov, const double* val, vo
 
 void dev_halo_unpack(int prec, void* g, int n, int ov, const void* all, int rank, int world, double* val,
                      cudaStream_t s) {
-    if (n < 1 || ov < 0 || ov > n) raise(PTG_ERR_GEOMETRY, "halo: need 0 <= overlap <= n");
+    if (n < 1 || ov < 0 || 2 * (size_t)ov > (size_t)n)   // top and bottom halo rows must not overlap
+        raise(PTG_ERR_GEOMETRY, "halo: need 0 <= 2 * overlap <= n");
     if (world < 1 || rank < 0 || rank >= world) raise(PTG_ERR_CONFIG, "halo: bad rank / world size");
     const size_t m = (size_t)ov * n, stride = halo_bytes(prec, n, ov);
     if (prec == PTG_C64)

@@ -986,6 +986,8 @@ void check_device(int device) {
 
 }  // namespace
 
+void check_device_public(int device) { check_device(device); }
+
 // ------------------------------------------------------------------ create
 // The solvers' work vectors are stream-ordered allocations (cudaMallocAsync).
 // With the default pool release threshold (0) every synchronisation hands the
@@ -1057,14 +1059,16 @@ std::unique_ptr<Plan> plan_create(const ptg_plan_desc& d) {
     p->scratch.alloc((kReduceBlocks + 2) * sizeof(double));
     PTG_CUDA(cudaMemsetAsync(p->scratch.p, 0, p->scratch.bytes, p->stream));
     p->flag.alloc(sizeof(unsigned long long));
-    p->hval.ensure(4 * sizeof(double));
+    // fixed size for the plan's lifetime: replayed host-eval graphs copy the value
+    // into this buffer, so it must never be reallocated (solvers use <= 8 doubles)
+    p->hval.ensure(kHvalDoubles * sizeof(double));
     if (d.data) plan_set_data_host(*p, d.data, d.data_dtype);
     PTG_CUDA(cudaStreamSynchronize(p->stream));
     return p;
 }
 
 // ------------------------------------------------------------------- data
-static void validate_and_amp(Plan& p) {
+void plan_refresh_amp(Plan& p) {
     const size_t len = (size_t)p.N * p.MM();
     p.amp.ensure(std::max<size_t>(1, len) * p.relem());
     unsigned long long init = ~0ull;
@@ -1095,7 +1099,7 @@ void plan_set_data_device(Plan& p, const void* data, int dtype) {
     const size_t len = (size_t)p.N * p.MM();
     p.inten.ensure(std::max<size_t>(1, len) * p.relem());
     if (len) dev_real_convert(p.prec, p.inten.p, dtype, data, len, p.stream);
-    validate_and_amp(p);
+    plan_refresh_amp(p);
 }
 
 // PTYF stack (image_io.hpp:10-20: "PTYF", u32 n, u32 channels, u32 0, then
@@ -1151,7 +1155,7 @@ void plan_load_ptyf(Plan& p, const char* path) {
         PTG_CUDA(cudaEventRecord(ev[b], p.stream));
         done += cnt;
     }
-    validate_and_amp(p);   // synchronises the stream
+    plan_refresh_amp(p);   // synchronises the stream
 }
 
 void plan_set_data_host(Plan& p, const void* data, int dtype) {
@@ -1184,7 +1188,7 @@ void plan_ensure(Plan& p, int metric) {
     }
     if (metric == PTG_DISTANCE && !p.amp_valid) {
         if (!p.inten_valid) raise(PTG_ERR_CONFIG, "plan has no diffraction data");
-        validate_and_amp(p);
+        plan_refresh_amp(p);
     }
     if (metric != PTG_DISTANCE && metric != PTG_INTENSITY) raise(PTG_ERR_CONFIG, "unknown metric kind");
 }
@@ -1381,13 +1385,16 @@ static void eval_host_banded(Plan& p, int metric, const double* z, const double*
             ++p.launches;
             f_done = f_end;
         }
-        // reduce blocks whose pixel rows no later frame reaches
+        // reduce blocks whose pixel rows no later frame reaches AND whose z / v
+        // rows are already on the device (rows < r1; every row after the last
+        // band) -- a scan that leaves uncovered rows must not reduce them early
         const int next_row = f_done < N ? p.pos_h[2 * f_done] : n;   // first row a pending frame touches
+        const int ready_row = b == K - 1 ? n : std::min(next_row, r1);
         int k_end = k_done;
         while (k_end < kPlaneBlocks) {
             const size_t hi = std::min(npairs, (size_t)(k_end + 1) * chunk);
             const size_t last_pix = hi ? std::min(nn - 1, 2 * hi - 1) : 0;
-            if (f_done < N && (int)(last_pix / n) >= next_row) break;
+            if ((int)(last_pix / n) >= ready_row) break;
             ++k_end;
         }
         if (k_end > k_done) {
@@ -1471,7 +1478,8 @@ void plan_eval_host(Plan& p, int metric, const double* z, const double* v, doubl
         auto key = [&] {
             return std::vector<const void*>{z, v, grad, (const void*)(intptr_t)metric, p.amp.p, p.inten.p, p.planes.p,
                                             p.zbuf.p, p.gbuf.p, p.vbuf.p, p.stage.p, p.stage_out.p, p.misfit.p,
-                                            p.color.p, p.probe_epi.p, p.amp_cl.p};
+                                            p.color.p, p.probe_epi.p, p.amp_cl.p, p.hval.p, p.value.p, p.dotp.p,
+                                            p.counter.p};
         };
         if (p.hg.exec && key() == p.hg.key) {
             PTG_CUDA(cudaGraphLaunch(p.hg.exec, p.stream));
@@ -1551,7 +1559,7 @@ void plan_simulate(Plan& p, const void* z) {
     else simulate_t<double>(p, z);
     p.inten_valid = true;
     p.amp_valid = false;
-    validate_and_amp(p);
+    plan_refresh_amp(p);
 }
 
 // ---------------------------------------------------------------- project
@@ -1705,7 +1713,7 @@ std::unique_ptr<Plan> plan_coarsen(Plan& f) {
         PTG_CUDA(cudaStreamSynchronize(f.stream));
         if (len) dev_restrict_data(dt, f.inten.p, f.N, f.M, c->inten.p, 1.0 / 16.0, c->stream);
         c->inten_valid = true;
-        validate_and_amp(*c);
+        plan_refresh_amp(*c);
     } else if (f.amp_valid) {
         c->amp.ensure(std::max<size_t>(1, len) * c->relem());
         PTG_CUDA(cudaStreamSynchronize(f.stream));

@@ -65,6 +65,7 @@ struct Chunk {
 
 constexpr int kTileW = 64;   // overlap-add gather tile: 64 x 8 pixels, 2 per thread (32 x 8 block)
 constexpr int kTileH = 8;
+constexpr int kHvalDoubles = 16;   // pinned host scalars per plan (never reallocated)
 
 struct Plan {
     int n = 0, M = 0, w = 0, N = 0, prec = PTG_C64, device = 0;
@@ -98,7 +99,7 @@ struct Plan {
     DevMem stash, misfit, dotp, value, scratch, flag, frame;
     DevMem counter;                  // last-block-done counter of the fused gather
     DevMem zbuf, vbuf, gbuf, stage;  // host-API working buffers
-    HostPinned hval;
+    HostPinned hval;   // kHvalDoubles, allocated once at plan creation
 
     // opt-in event timing of the frame kernel / gather (ptg_plan_set_timing)
     struct EvPair { cudaEvent_t a = nullptr, b = nullptr; int kind = 0; };
@@ -171,12 +172,24 @@ struct LaunchScope {
 };
 
 std::unique_ptr<Plan> plan_create(const ptg_plan_desc& d);
+// status 4 unless `device` is a usable sm_100 device (selects it)
+void check_device_public(int device);
 // coarse plan built on device from a fine one (patch-model coarsening)
 std::unique_ptr<Plan> plan_coarsen(Plan& fine);
 void plan_set_data_host(Plan& p, const void* data, int dtype);
 void plan_set_data_device(Plan& p, const void* data, int dtype);
 void plan_load_ptyf(Plan& p, const char* path);   // PTYF stack file, streamed upload
 void plan_ensure(Plan& p, int metric);   // make amp / inten valid for metric
+// intensities rewritten on device: d >= 0 check + amplitudes (checkPattern)
+void plan_refresh_amp(Plan& p);
+// addNoise (forward.cpp:56-86) in place on the plan's data; uniforms_host =
+// NULL draws Philox4x64-10 (seed), else 2 N M^2 uniforms in the reference's order
+void plan_add_noise(Plan& p, double level, unsigned long long seed, const double* uniforms_host);
+// Poisson photon noise at `photons` per pattern (counter-based, seed)
+void plan_add_poisson(Plan& p, double photons, unsigned long long seed);
+// raw Philox4x64-10 blocks: out[4 b + k] = philox(ctr + (b, 0, 0, 0), key)[k]
+void dev_philox_raw(unsigned long long* out, size_t nblocks, const unsigned long long ctr[4],
+                    const unsigned long long key[2], cudaStream_t s);
 
 // objective + gradient on device buffers (plan precision); grad may be null
 void plan_eval(Plan& p, int metric, const void* z, const void* v, void* grad, double* value_dev);

@@ -166,7 +166,7 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     // synchronisation (same kernels and partitions as plan_nonfinite / dnorm)
     double z0sq = 0.0, gsq = 0.0;
     {
-        p.hval.ensure(8 * sizeof(double));
+        static_assert(kHvalDoubles >= 8, "hval holds the solver scalars");
         double* hv = p.hval.as<double>();
         double* vd = p.value.as<double>();
         dev_nonfinite(p.prec, g.p, len, p.flag.as<int>(), p.stream);
@@ -197,7 +197,7 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     std::deque<int> order;
     DVec ws;   // fused-kernel scratch (two-loop partials / pair statistics / products)
     double* wsd = nullptr;
-    p.hval.ensure(8 * sizeof(double));
+    static_assert(kHvalDoubles >= 8, "hval holds the solver scalars");
     // pinned results of an iteration: [0] first trial's value, [1..5] pair
     // statistics, [9..] compact-mode products -- one block so the graph-replayed
     // iteration reads them back with a single copy

@@ -196,6 +196,23 @@ class Plan:
     def simulate_device(self, z):
         check(lib().ptg_simulate_device(self._h, _vp(z)))
 
+    def add_noise(self, level: float, seed: int = 0, uniforms=None):
+        """addNoise (forward.hpp:44-48) on the resident data, on the GPU.
+        uniforms: None = Philox4x64-10 stream; else 2 N M^2 uniforms in the
+        reference's draw order (its std::mt19937_64 stream)."""
+        u = None if uniforms is None else np.ascontiguousarray(uniforms, dtype=np.float64)
+        check(lib().ptg_add_noise(self._h, float(level), int(seed), _vp(u)))
+
+    def add_poisson(self, photons: float, seed: int = 4):
+        """Poisson photon noise at `photons` per pattern, on the GPU."""
+        check(lib().ptg_add_poisson(self._h, float(photons), int(seed)))
+
+    def data_host(self, metric: int = INTENSITY) -> np.ndarray:
+        """The resident intensities (metric INTENSITY) or amplitudes, as float64 [N, M, M]."""
+        out = np.empty((self.N, self.M, self.M), np.float64)
+        check(lib().ptg_plan_get_data(self._h, int(metric), out.ctypes.data))
+        return out
+
     # -- solvers
     def pie(self, z0, gamma: float = 0.0, sweeps: int = 1,
             max_weighted: float = float("inf")) -> SolverReport:

@@ -122,6 +122,8 @@ class HaloExchange:
     def __init__(self, n: int, overlap: int, dtype, device, group=None):
         import torch
         import torch.distributed as dist
+        if overlap < 0 or 2 * overlap > n:   # top and bottom halo rows would overlap
+            raise ValueError(f"halo: need 0 <= 2 * overlap <= n (overlap {overlap}, n {n})")
         self.n, self.ov, self.group = n, overlap, group
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         self.dtype = dtype
