@@ -151,6 +151,10 @@ int ptg_add_noise(ptg_plan *plan, double level, uint64_t seed, const double *uni
  * k ~ Poisson(lambda) (inversion below 10, PTRS transformed rejection above),
  * uniforms from Philox4x64-10 with counter (pixel, pattern, 2, block). */
 int ptg_add_poisson(ptg_plan *plan, double photons, uint64_t seed);
+/* the first `count` rng::uniform01 draws (rng.hpp:14-16: top 53 bits of a
+ * std::mt19937_64 draw x 2^-53) of an engine seeded with `seed`, on the host
+ * (no device needed): the seeded synthetic inputs of SURVEY 8(d) */
+int ptg_uniform01_stream(uint64_t seed, size_t count, double *out);
 /* raw Philox4x64-10 output on `device`: out[4 b + k] = word k of
  * philox(counter (ctr[0] + b, ctr[1], ctr[2], ctr[3]), key), b < nblocks
  * (host out; for pinning the generator against numpy.random.Philox) */

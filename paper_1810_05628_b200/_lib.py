@@ -104,7 +104,7 @@ EXPORTS = [
     "ptg_plan_set_data_device", "ptg_plan_load_ptyf", "ptg_plan_get_data", "ptg_plan_info", "ptg_plan_launch_count",
     "ptg_plan_set_timing", "ptg_plan_get_timing",
     "ptg_eval", "ptg_eval_device", "ptg_project_modulus", "ptg_simulate", "ptg_simulate_device",
-    "ptg_add_noise", "ptg_add_poisson", "ptg_philox4x64",
+    "ptg_add_noise", "ptg_add_poisson", "ptg_philox4x64", "ptg_uniform01_stream",
     "ptg_pie", "ptg_pie_sweep_device",
     "ptg_restrict_field", "ptg_prolong_field", "ptg_restrict_data",
     "ptg_restrict_field_device", "ptg_prolong_field_device", "ptg_restrict_data_device",
@@ -150,6 +150,7 @@ def lib() -> C.CDLL:
     L.ptg_add_noise.argtypes = [_vp, C.c_double, C.c_uint64, _vp]
     L.ptg_add_poisson.argtypes = [_vp, C.c_double, C.c_uint64]
     L.ptg_philox4x64.argtypes = [C.c_int, _vp, _vp, C.c_size_t, _vp]
+    L.ptg_uniform01_stream.argtypes = [C.c_uint64, C.c_size_t, _vp]
     L.ptg_restrict_field.argtypes = [_vp, C.c_int, _vp]
     L.ptg_prolong_field.argtypes = [_vp, C.c_int, _vp]
     L.ptg_restrict_data.argtypes = [_vp, C.c_int, C.c_int, _vp]

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <limits>
 #include <new>
+#include <random>
 #include <string>
 
 #include "plan.cuh"
@@ -303,6 +304,13 @@ int ptg_add_poisson(ptg_plan* plan, double photons, uint64_t seed) {
         ptg::Plan& p = P(plan);
         ptg::plan_add_poisson(p, photons, (unsigned long long)seed);
         PTG_CUDA(cudaStreamSynchronize(p.stream));
+    });
+}
+
+int ptg_uniform01_stream(uint64_t seed, size_t count, double* out) {
+    return guard([&] {
+        std::mt19937_64 eng(seed);
+        for (size_t i = 0; i < count; ++i) out[i] = (double)(eng() >> 11) * 0x1.0p-53;
     });
 }
 

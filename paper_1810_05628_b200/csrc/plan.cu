@@ -864,7 +864,7 @@ int colour_positions(const Plan& p, std::vector<int>& color) {
 // a plain streaming reduction beats the list-driven gather by far.
 bool choose_planes(Plan& p) {
     if (p.N == 0 || p.mp) return false;
-    static const bool off = getenv("PTG_NO_PLANES") && getenv("PTG_NO_PLANES")[0] == '1';   // A/B switch
+    const bool off = getenv("PTG_NO_PLANES") && getenv("PTG_NO_PLANES")[0] == '1';   // A/B switch (read per plan)
     if (off) return false;
     std::vector<int> color;
     const int ncol = colour_positions(p, color);
@@ -903,7 +903,10 @@ void build_chunks(Plan& p) {
         return;
     }
     const size_t per = (size_t)p.w * stash_pitch(p.w) * p.celem();
-    const size_t budget = (size_t)2 << 30;   // stash bytes per chunk
+    // stash bytes per chunk: 2 GiB; PTG_STASH_BUDGET_MB lowers it (read per
+    // plan) so tests can drive the multi-chunk path with small problems
+    size_t budget = (size_t)2 << 30;
+    if (const char* e = getenv("PTG_STASH_BUDGET_MB")) budget = std::max<size_t>(1, (size_t)atoll(e)) << 20;
     int cs = p.N > 0 ? (int)std::min<size_t>((size_t)p.N, std::max<size_t>(1, budget / per)) : 1;
     p.chunk_size = cs;
     p.chunks.clear();

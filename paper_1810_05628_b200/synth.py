@@ -13,8 +13,11 @@ seeded synthetic objects instead, reproduced here:
   product, the oracle in tests), optional Poisson noise at a photon budget
 
 Inputs are generated once on the host and fed byte-identically to the GPU
-and to the CPU oracle.  RNG: numpy PCG64 with fixed seeds (object 1/2,
-jitter 3, Poisson 4), documented in DESIGN.md.
+and to the CPU oracle.  RNG (SURVEY 8(d)): the reference's std::mt19937_64 +
+rng::uniform01 (rng.hpp:14-16, via ptg_uniform01_stream) with fixed seeds
+(object magnitude 1 / phase 2, jitter 3); Poisson noise is drawn on the GPU
+from Philox4x64-10 keyed by seed 4 (ptg_add_poisson).  A C++ user regenerates
+the same fields with the reference's own rng.hpp.
 """
 from __future__ import annotations
 
@@ -22,6 +25,7 @@ from dataclasses import dataclass
 from typing import Optional
 
 import numpy as np
+import scipy.fft as sfft
 
 
 @dataclass(frozen=True)
@@ -65,19 +69,31 @@ CONFIGS = {
 }
 
 
-def smooth_field(n: int, sigma: float, rng: np.random.Generator) -> np.ndarray:
-    """Uniform noise, periodically Gaussian-filtered (sigma px), min-max to [0, 1]."""
-    u = rng.uniform(size=(n, n))
+def uniform01(seed: int, count: int) -> np.ndarray:
+    """rng::uniform01 draws of std::mt19937_64(seed) (rng.hpp:14-16), row-major."""
+    from paper_1810_05628_b200 import _lib
+    out = np.empty(count, np.float64)
+    _lib.check(_lib.lib().ptg_uniform01_stream(int(seed), count, out.ctypes.data))
+    return out
+
+
+def smooth_field(n: int, sigma: float, seed: int) -> np.ndarray:
+    """Uniform noise (mt19937_64(seed), row-major), periodically Gaussian-filtered
+    (sigma px), min-max to [0, 1]."""
+    u = uniform01(seed, n * n).reshape(n, n)
     f = np.fft.fftfreq(n)
     k = np.exp(-2.0 * np.pi ** 2 * sigma ** 2 * (f[:, None] ** 2 + f[None, :] ** 2))
-    s = np.real(np.fft.ifft2(np.fft.fft2(u) * k))
+    # scipy's pocketfft with all host threads (8192^2: 0.3 s vs 4.6 s per
+    # transform for numpy's single-threaded one); rows are transformed
+    # independently, so the result does not depend on the thread count
+    s = np.real(sfft.ifft2(sfft.fft2(u, workers=-1) * k, workers=-1))
     lo, hi = s.min(), s.max()
     return (s - lo) / (hi - lo) if hi > lo else np.zeros_like(s)
 
 
 def make_object(n: int, sigma: float, seed_mag: int = 1, seed_phase: int = 2) -> np.ndarray:
-    mag = 0.5 + 0.5 * smooth_field(n, sigma, np.random.default_rng(seed_mag))
-    ph = (2.0 * smooth_field(n, sigma, np.random.default_rng(seed_phase)) - 1.0) * (np.pi / 4)
+    mag = 0.5 + 0.5 * smooth_field(n, sigma, seed_mag)
+    ph = (2.0 * smooth_field(n, sigma, seed_phase) - 1.0) * (np.pi / 4)
     return (mag * np.exp(1j * ph)).astype(np.complex128)
 
 
@@ -97,22 +113,11 @@ def raster(n: int, w: int, steps: int, step: int, jitter: int = 0, seed: int = 3
             pos.append((i * step, jj * step))
     pos = np.array(pos, dtype=np.int64)
     if jitter:
-        rng = np.random.default_rng(seed)
-        pos = pos + rng.integers(-jitter, jitter + 1, size=pos.shape)
+        # U{-jitter..jitter} per coordinate, (row, col) per position in scan order
+        u = uniform01(seed, pos.size).reshape(pos.shape)
+        pos = pos + np.floor(u * (2 * jitter + 1)).astype(np.int64) - jitter
     pos = np.clip(pos, 0, n - w)
     return pos.astype(np.int32)
-
-
-def poisson(data: np.ndarray, photons: float, seed: int = 4) -> np.ndarray:
-    """Poisson counts at `photons` per pattern, rescaled back to intensity units."""
-    rng = np.random.default_rng(seed)
-    d = np.asarray(data, dtype=np.float64)
-    tot = d.reshape(d.shape[0], -1).sum(axis=1)
-    scale = np.where(tot > 0, photons / np.maximum(tot, 1e-300), 0.0)[:, None, None]
-    counts = rng.poisson(d * scale)
-    with np.errstate(invalid="ignore", divide="ignore"):
-        out = np.where(scale > 0, counts / np.where(scale > 0, scale, 1.0), 0.0)
-    return out
 
 
 def make_inputs(cfg: Config):

@@ -1,0 +1,157 @@
+"""GPU parity at BASELINE's real sizes (configs 3-5) and on the multi-chunk
+overlap-add path, against the CPU oracle (objectives.cpp:52-118 restated).
+
+Config 3 (n=1024, M=128, jittered) and config 4 (n=4096, M=256, Poisson) run
+in full; config 5 (n=8192, 27,556 patterns) is checked on a sub-problem of
+its geometry against the oracle and in full through size-independent
+properties (additivity over position subsets, determinism, the shift
+identity).  Tolerances: complex64 objective 1e-5 relative, gradient 1e-4
+relative L2 (BASELINE.json north_star).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import rand_field, rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+C64_VAL, C64_GRAD = 1e-5, 1e-4
+
+
+def _r64(a):
+    return np.asarray(a).astype(np.complex64).astype(np.complex128)
+
+
+def _case(oracle, cfg, pos=None, n=None, obj=None, seed=5, photons=None):
+    """(oracle problem, z, v, float32 data, probe, pos, n) for cfg's geometry."""
+    from paper_1810_05628_b200 import synth
+    o, probe, p = synth.make_inputs(cfg) if obj is None else (obj, synth.make_probe(cfg.M, cfg.sigma_probe, cfg.a), pos)
+    n = cfg.n if n is None else n
+    pos = p if pos is None else pos
+    probe = _r64(probe)
+    o = _r64(o[:n, :n])
+    oracle.set_threads(os.cpu_count() or 1)
+    data = oracle.simulate(n, cfg.M, cfg.w, pos, o, probe)
+    photons = cfg.photons if photons is None else photons
+    if photons:
+        data = oracle.add_poisson(data, photons, seed=4)
+    data = data.astype(np.float32)
+    z = _r64(o * 0.9 + 0.05 * rand_field(n, seed))
+    v = _r64(0.01 * rand_field(n, seed + 1))
+    prob = oracle.Problem(n, cfg.M, cfg.w, pos, data.astype(np.float64), probe)
+    return prob, z, v, data, probe, pos, n
+
+
+def _check(plan, prob, oracle, z, v):
+    gv, gg = plan.evaluate(z, v)
+    wv, wg = oracle.evaluate(prob, z, v)
+    assert rel(gv, wv) <= C64_VAL, (gv, wv)
+    assert rel_l2(gg, wg) <= C64_GRAD, rel_l2(gg, wg)
+    return gv, gg
+
+
+def test_config3_full(oracle):
+    from paper_1810_05628_b200 import Plan, synth
+    cfg = synth.CONFIGS[3]
+    prob, z, v, data, probe, pos, n = _case(oracle, cfg)
+    plan = Plan(n, cfg.M, cfg.w, pos, data, probe, precision="c64")
+    _check(plan, prob, oracle, z, v)
+    _check(plan, prob, oracle, z, None)
+    plan.close()
+
+
+def test_config4_full(oracle):
+    from paper_1810_05628_b200 import Plan, synth
+    cfg = synth.CONFIGS[4]
+    prob, z, v, data, probe, pos, n = _case(oracle, cfg)
+    plan = Plan(n, cfg.M, cfg.w, pos, data, probe, precision="c64")
+    _check(plan, prob, oracle, z, v)
+    plan.close()
+
+
+def test_config4_device_poisson_matches_oracle_sampler(oracle):
+    """The bench's data path (GPU forward operator + GPU Poisson) = the oracle's."""
+    from paper_1810_05628_b200 import Plan, synth
+    cfg = synth.CONFIGS[4]
+    obj, probe, pos = synth.make_inputs(cfg)
+    sub = pos[:61 * 3]                     # three scan rows
+    probe, obj = _r64(probe), _r64(obj)
+    plan = Plan(cfg.n, cfg.M, cfg.w, sub, None, probe, precision="c128")
+    plan.simulate(obj, copy_out=False)
+    plan.add_poisson(cfg.photons, seed=4)
+    got = plan.data_host()
+    want = oracle.add_poisson(oracle.simulate(cfg.n, cfg.M, cfg.w, sub, obj, probe), cfg.photons, seed=4)
+    assert np.isclose(got, want, rtol=1e-9, atol=0).mean() > 0.9999
+    plan.close()
+
+
+@pytest.mark.parametrize("budget_mb", [48, 200])
+def test_multichunk_stash_matches_single(oracle, monkeypatch, budget_mb):
+    """Stash budget lowered so the overlap-add runs in >= 3 chunks
+    (accumulating gathers + separate shift / finalize kernels)."""
+    from paper_1810_05628_b200 import Plan, synth
+    cfg = synth.CONFIGS[3]
+    prob, z, v, data, probe, pos, n = _case(oracle, cfg)
+    monkeypatch.setenv("PTG_NO_PLANES", "1")
+    monkeypatch.setenv("PTG_STASH_BUDGET_MB", str(budget_mb))
+    plan = Plan(n, cfg.M, cfg.w, pos, data, probe, precision="c64")
+    _check(plan, prob, oracle, z, v)
+    _check(plan, prob, oracle, z, None)
+    plan.close()
+
+
+def test_config5_subproblem(oracle):
+    """Config 5's probe / step / noise on the top-left 2048^2 window (38 x 38 positions)."""
+    from paper_1810_05628_b200 import Plan, synth
+    cfg = synth.CONFIGS[5]
+    S = 2048
+    steps = (S - cfg.w) // cfg.step + 1
+    obj = synth.make_object(S, cfg.sigma_obj)
+    pos = synth.raster(S, cfg.w, steps, cfg.step)
+    prob, z, v, data, probe, pos, n = _case(oracle, cfg, pos=pos, n=S, obj=obj)
+    plan = Plan(n, cfg.M, cfg.w, pos, data, probe, precision="c64")
+    _check(plan, prob, oracle, z, v)
+    plan.close()
+
+
+def test_config5_full_properties():
+    """Full config 5 on the GPU: (1) bitwise determinism, (2) additivity: the
+    evaluation over all 27,556 positions equals the sum of the evaluations
+    over the even and odd scan rows, (3) the MG/OPT shift identity
+    value(v) = value(0) - <v,z>, grad(v) = grad(0) - v."""
+    import torch
+
+    from paper_1810_05628_b200 import Plan, synth
+    cfg = synth.CONFIGS[5]
+    obj, probe, pos = synth.make_inputs(cfg)
+    rows = pos.reshape(cfg.steps, cfg.steps, 2)
+    plans = []
+    for sel in (pos, rows[0::2].reshape(-1, 2), rows[1::2].reshape(-1, 2)):
+        p = Plan(cfg.n, cfg.M, cfg.w, sel, None, probe, precision="c64")
+        p.simulate(obj, copy_out=False)
+        plans.append(p)
+    g = torch.Generator(device="cpu").manual_seed(3)
+    z = (torch.from_numpy(obj).to(torch.complex64) * 0.9).cuda()
+    z += 0.05 * torch.complex(torch.rand(cfg.n, cfg.n, generator=g) - 0.5,
+                              torch.rand(cfg.n, cfg.n, generator=g) - 0.5).cuda()
+    grads = [torch.empty_like(z) for _ in plans]
+    vals = [p.evaluate_device(z, gr) for p, gr in zip(plans, grads)]
+    # (1) determinism
+    g2 = torch.empty_like(z)
+    assert plans[0].evaluate_device(z, g2) == vals[0]
+    assert torch.equal(g2, grads[0])
+    # (2) additivity
+    assert rel(vals[0], vals[1] + vals[2]) <= 1e-6
+    gsum = grads[1] + grads[2]
+    assert float(torch.linalg.vector_norm(grads[0] - gsum) / torch.linalg.vector_norm(grads[0])) <= 1e-5
+    # (3) shift
+    v = 0.01 * torch.complex(torch.rand(cfg.n, cfg.n, generator=g), torch.rand(cfg.n, cfg.n, generator=g)).cuda()
+    gv = torch.empty_like(z)
+    val_v = plans[0].evaluate_device(z, gv, v=v)
+    dot = float(torch.sum(v.real.double() * z.real.double() + v.imag.double() * z.imag.double()))
+    assert rel(val_v, vals[0] - dot) <= 1e-9
+    assert float(torch.linalg.vector_norm(gv - (grads[0] - v)) / torch.linalg.vector_norm(gv)) <= 1e-6
+    for p in plans:
+        p.close()

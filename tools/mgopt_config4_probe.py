@@ -18,7 +18,7 @@ plan = Plan(cfg.n, cfg.M, cfg.w, pos, None, probe, precision=cfg.precision)
 plan.set_stream(stream.cuda_stream)
 host = plan.simulate(obj, copy_out=bool(cfg.photons))
 if cfg.photons:
-    plan.set_data(synth.poisson(host, cfg.photons, seed=4))
+    plan.add_poisson(cfg.photons, seed=4)
 h = Hierarchy(plan, cfg.depth)
 z = torch.ones(cfg.n, cfg.n, dtype=torch.complex64, device="cuda")
 g = torch.empty_like(z)
