@@ -1,0 +1,382 @@
+// frame_rmw.cuh — persistent cluster frame kernel with an in-place,
+// dependency-ordered overlap-add (complex64, M = Q L = 128 / 256, w == M).
+//
+// The per-frame computation is frame_cl_kernel's (frame_cl.cuh: gather fused
+// with the column DIF butterflies over distributed shared memory, register
+// FFT_L passes, spectral operator + fp64 misfit, inverse passes, conj(P)
+// epilogue; reference objectives.cpp:59-103).  What changes is where the
+// contribution goes.  frame_cl_kernel stores every frame's M x M contribution
+// (512 KiB at M = 256) to a per-position stash in HBM and a separate gather
+// sums the stashes: 2 x 14.4 GB of HBM traffic per config-5 evaluation on top
+// of the 8.3 GB the evaluation needs.  Here the frame adds its contribution
+// straight into the gradient:
+//
+//   * the plan orders the positions (host, plan.cu build_rmw): groups of
+//     consecutive window rows, inside a group greedy colour classes of
+//     pairwise non-overlapping windows, class by class.  That order is the
+//     summation order of every pixel -- fixed by the geometry, so results are
+//     bitwise reproducible run to run (no float atomics: every update is a
+//     plain load + add + store by the one frame that owns the pixel then);
+//   * frame k may update the gradient only after every EARLIER overlapping
+//     frame has finished its update: a per-frame completion counter (one
+//     release-increment per CTA, CUTLASS GenericBarrier style) that the
+//     CTAs of frame k acquire before their read-modify-write.  Overlapping
+//     frames are >= one colour class apart in the order (~25 frames for
+//     config 5), so the wait almost never blocks;
+//   * frames are handed out by an atomic counter (persistent grid of
+//     co-resident clusters; a frame is only ever waited on after a running
+//     cluster claimed it, so the protocol cannot deadlock), and the gradient
+//     rows being updated (window height x object width) stay L2-resident as
+//     the scan advances: HBM sees the amplitudes, the object and the
+//     gradient about once.
+//
+// The gradient is initialised (= -v for the MG/OPT shift, else 0) and the
+// counters zeroed by k_rmw_init before the launch; k_finalize forms the value.
+#pragma once
+
+#include "frame_cl.cuh"
+
+namespace ptg {
+
+struct RmwArgs {
+    const int* order;     // [N] dispatch / summation order -> position index
+    const int* dep_off;   // [N + 1] CSR offsets over order indices
+    const int* dep_idx;   // order indices of the earlier overlapping frames
+    unsigned* done;       // [N] per order index: CTAs finished (Q = complete), zeroed per evaluation
+    unsigned* work;       // dispatch counter, zeroed per evaluation
+    float2* grad;         // gradient, row pitch a.n
+    int N;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_gpu_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, unsigned v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_f2(uint32_t addr, float2 v) {
+    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+    const float2 lo = cadd(make_float2(a.x, a.y), make_float2(b.x, b.y));
+    const float2 hi = cadd(make_float2(a.z, a.w), make_float2(b.z, b.w));
+    return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+
+template <int Q, int L, int OP, bool PROBE>
+__global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
+    frame_rmw_kernel(FrameArgs<float> a, const float* __restrict__ amp_perm, const float2* __restrict__ tw_g,
+                     const float2* __restrict__ probe_epi, RmwArgs r) {
+    namespace cg = cooperative_groups;
+    constexpr int M = Q * L, NT = M, PM = cl_pitch<Q, L>(), NPC = L / Q, AP = cl_amp_pitch<Q, L>();
+    static_assert(cl_amp_staged<Q, L>(), "the persistent kernel stages amplitudes");
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ __align__(16) unsigned char cl_smem[];
+    float2* buf = reinterpret_cast<float2*>(cl_smem);   // [L][PM]: this CTA's frame rows
+    float2* tw = buf + L * PM;                           // W_M^i, i < M
+    float* amp_s = reinterpret_cast<float*>(tw + M);     // [L][AP]
+    __shared__ double red[NT / 32];
+    __shared__ __align__(8) unsigned long long bar_a, bar_g;
+    __shared__ int s_item;
+
+    const int q = (int)cl.block_rank();
+    const int t = threadIdx.x;
+    const int n = a.n;
+    if (t == 0) {
+        mbar_init(&bar_g, 1);
+        mbar_init(&bar_a, 1);
+        fence_mbarrier_init();
+    }
+    for (int i = t; i < M; i += NT) tw[i] = __ldg(tw_g + i);
+    int next = 0;
+    if (q == 0 && t == 0) next = (int)atomicAdd(r.work, 1u);
+    __syncthreads();
+    const int m = t % L, g = t / L;
+    const int rr = t % L, qq = t / L;
+    const uint32_t bar_g_u = smem_u32(&bar_g), buf_u = smem_u32(buf);
+    uint32_t ph = 0;
+
+#pragma unroll 1
+    for (;;) {
+        // this frame's gather bytes, then the item handed to every CTA of the
+        // cluster; the full cluster barrier also orders every CTA's previous
+        // epilogue (reads of its own rows) before the pushes of this frame
+        if (t == 0) mbar_arrive_expect_tx(&bar_g, (uint32_t)(L * M * sizeof(float2)));
+        if (q == 0 && t == 0) {
+#pragma unroll
+            for (int s = 0; s < Q; ++s) st_cluster_u32(mapa_u32(smem_u32(&s_item), s), (unsigned)next);
+            next = (int)atomicAdd(r.work, 1u);   // the following frame, claimed ahead
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        const int k = s_item;
+        if (k >= r.N) break;
+        const int j = __ldg(r.order + k);
+        const int2 pj = a.pos[j];
+
+        if (t < 32) {   // this CTA's L permuted amplitude rows, one bulk copy per row
+            const float* src = amp_perm + (size_t)j * M * M + (size_t)q * L * M;
+            if (t == 0) mbar_arrive_expect_tx(&bar_a, L * M * sizeof(float));
+            __syncwarp();
+            for (int r2 = t; r2 < L; r2 += 32)
+                tma_bulk_g2s(amp_s + r2 * AP, src + (size_t)r2 * M, M * sizeof(float), &bar_a);
+        }
+
+        // gather fused with the column DIF butterflies (frame_cl.cuh)
+        float2 x[L];
+        {
+            constexpr int BT = 16 / Q;
+            const float2* zc = a.z + (size_t)pj.x * n + pj.y + t;
+#pragma unroll 1
+            for (int b = 0; b < NPC; b += BT) {
+                float2 zv[BT * Q], pv[BT * Q];
+#pragma unroll
+                for (int i = 0; i < BT; ++i)
+#pragma unroll
+                    for (int s = 0; s < Q; ++s) {
+                        const int row = q * NPC + b + i + L * s;
+                        zv[i * Q + s] = zc[(size_t)row * n];
+                        if constexpr (PROBE) pv[i * Q + s] = __ldg(a.probe + (size_t)row * M + t);
+                    }
+#pragma unroll
+                for (int i = 0; i < BT; ++i) {
+                    const int rw = q * NPC + b + i;
+                    float2 v[Q];
+#pragma unroll
+                    for (int s = 0; s < Q; ++s) v[s] = PROBE ? cmul(pv[i * Q + s], zv[i * Q + s]) : zv[i * Q + s];
+                    dft_q<Q>(v);
+#pragma unroll
+                    for (int s = 1; s < Q; ++s) v[s] = cmul(tw[rw * s], v[s]);
+#pragma unroll
+                    for (int s = 0; s < Q; ++s)
+                        st_async_f2(mapa_u32(smem_u32(buf + rw * PM + t), s), v[s], mapa_u32(bar_g_u, s));
+                }
+            }
+        }
+        mbar_wait(&bar_g, ph);   // all Q senders' rows have landed in this CTA
+
+        double acc = 0.0;
+#pragma unroll 1
+        for (int pass = 0; pass < 4; ++pass) {
+            if (pass == 0 || pass == 3) {
+#pragma unroll
+                for (int kk = 0; kk < L; ++kk) x[kk] = buf[kk * PM + t];
+                if (pass == 3) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+            } else if (pass == 1) {
+#pragma unroll
+                for (int c = 0; c < L; c += 2) {
+                    const float4 v = *reinterpret_cast<const float4*>(&buf[rr * PM + qq * L + c]);
+                    x[c] = make_float2(v.x, v.y);
+                    x[c + 1] = make_float2(v.z, v.w);
+                }
+            }
+            reg_fft<L, false>(x);
+            if (pass == 0) {
+#pragma unroll
+                for (int kk = 0; kk < L; ++kk) buf[kk * PM + t] = x[kk];
+                __syncthreads();
+#pragma unroll 2
+                for (int i = 0; i < NPC; ++i) {
+                    float2* row = buf + (g + Q * i) * PM + m;
+                    float2 v[Q];
+#pragma unroll
+                    for (int s = 0; s < Q; ++s) v[s] = row[L * s];
+                    dft_q<Q>(v);
+#pragma unroll
+                    for (int s = 1; s < Q; ++s) v[s] = cmul(tw[m * s], v[s]);   // W_M^{m s} from shared memory
+#pragma unroll
+                    for (int s = 0; s < Q; ++s) row[L * s] = v[s];
+                }
+                __syncthreads();
+            } else if (pass == 1) {
+                float af[4] = {0.f, 0.f, 0.f, 0.f};
+                mbar_wait(&bar_a, ph);
+#pragma unroll
+                for (int c = 0; c < L; c += 4) {
+                    const float4 A4 = *reinterpret_cast<const float4*>(amp_s + rr * AP + qq * L + c);
+                    const float Av[4] = {A4.x, A4.y, A4.z, A4.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float2 W = x[c + u];
+                        const float Am = Av[u];
+                        float2 R;
+                        if constexpr (OP == OP_INTENSITY) {
+                            const float rs = (W.x * W.x + W.y * W.y) - Am;
+                            af[u] = fmaf(rs, rs, af[u]);
+                            R = make_float2(W.x * rs, W.y * rs);
+                        } else {
+                            const float m2 = fmaf(W.x, W.x, W.y * W.y);
+                            const bool nz = m2 >= 1.17549435e-38f;
+                            const float inv = nz ? rsqrt_ftz(m2) : 0.f;
+                            const float dl = fmaf(m2, inv, -Am);
+                            af[u] = fmaf(dl, dl, af[u]);
+                            const float s = fmaf(-Am, inv, 1.f);
+                            R = make_float2(fmaf(W.x, s, nz ? 0.f : -Am), W.y * s);
+                        }
+                        x[c + u] = make_float2(R.x, -R.y);
+                    }
+                }
+                acc = ((double)af[0] + (double)af[1]) + ((double)af[2] + (double)af[3]);
+            } else if (pass == 2) {
+#pragma unroll
+                for (int c = 0; c < L; c += 2)
+                    *reinterpret_cast<float4*>(&buf[rr * PM + qq * L + c]) =
+                        make_float4(x[c].x, x[c].y, x[c + 1].x, x[c + 1].y);
+                __syncthreads();
+#pragma unroll 2
+                for (int i = 0; i < NPC; ++i) {
+                    float2* row = buf + (g + Q * i) * PM + m;
+                    float2 v[Q];
+#pragma unroll
+                    for (int s = 0; s < Q; ++s) v[s] = row[L * s];
+#pragma unroll
+                    for (int s = 1; s < Q; ++s) v[s] = cmul(tw[m * s], v[s]);   // W_M^{m s} from shared memory
+                    dft_q<Q>(v);
+#pragma unroll
+                    for (int s = 0; s < Q; ++s) row[L * s] = v[s];
+                }
+                __syncthreads();
+            } else {
+                asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+#pragma unroll
+                for (int kk = 0; kk < L; ++kk)   // remote row (kk % NPC) Q + q of CTA kk / NPC
+                    st_cluster_f2(mapa_u32(buf_u + (uint32_t)((((kk % NPC) * Q + q) * PM + t) * sizeof(float2)),
+                                           kk / NPC),
+                                  x[kk]);
+            }
+        }
+        if constexpr (PROBE) {
+#pragma unroll
+            for (int i = 0; i < NPC; ++i)
+#pragma unroll
+                for (int s = 0; s < Q; ++s) x[i * Q + s] = __ldg(probe_epi + (size_t)(q * NPC + i + L * s) * M + t);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if ((t & 31) == 0) red[t / 32] = acc;
+        cl.sync();   // every push has landed; no remote access to this CTA's rows until the next frame
+        if (t == 0) {
+            double s = 0.0;
+#pragma unroll
+            for (int i = 0; i < NT / 32; ++i) s += red[i];
+            constexpr int MPP = M / 32;
+            a.misfit[(size_t)j * MPP + q] = (OP == OP_DISTANCE) ? s / (2.0 * (double)M * (double)M) : 0.5 * s;
+            if constexpr (MPP > Q) a.misfit[(size_t)j * MPP + Q + q] = 0.0;
+        }
+
+        // (A) contributions, in place: buf row i Q + s holds object row
+        //     pj.x + q NPC + i + L s (columns pj.y .. pj.y + M), column t
+        const float sc = (OP == OP_DISTANCE) ? 1.f / (float(M) * float(M)) : 2.f;
+#pragma unroll
+        for (int i = 0; i < NPC; ++i) {
+            const int rw = q * NPC + i;
+            float2 v[Q];
+#pragma unroll
+            for (int s = 0; s < Q; ++s) v[s] = buf[(i * Q + s) * PM + t];
+#pragma unroll
+            for (int s = 1; s < Q; ++s) v[s] = cmul(tw[rw * s], v[s]);
+            dft_q<Q>(v);
+#pragma unroll
+            for (int s = 0; s < Q; ++s)
+                buf[(i * Q + s) * PM + t] = PROBE ? epi_contrib_pre(v[s], x[i * Q + s]) : epi_contrib(v[s], sc);
+        }
+        // (B) every earlier overlapping frame has finished its update
+        {
+            const int d0 = __ldg(r.dep_off + k), d1 = __ldg(r.dep_off + k + 1);
+            for (int d = d0 + t; d < d1; d += NT) {
+                const unsigned* f = r.done + __ldg(r.dep_idx + d);
+                while (ld_acquire_gpu(f) < (unsigned)Q) __nanosleep(64);
+            }
+        }
+        __syncthreads();
+        // (C) read-modify-write of this CTA's L object rows, coalesced; every
+        //     load in flight at once (x[] is free again)
+        float2* G0 = r.grad + (size_t)pj.x * n + pj.y;
+        if ((pj.y & 1) == 0) {
+            constexpr int HW = M / 2, PER = L * HW / NT, HALF = PER / 2;   // float4 (pixel pairs) per thread
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float4 gv[HALF];
+#pragma unroll
+                for (int u = 0; u < HALF; ++u) {
+                    const int e = t + NT * (h * HALF + u), row = e / HW, c2 = e % HW;
+                    const int orow = q * NPC + row / Q + L * (row % Q);
+                    gv[u] = __ldcg(reinterpret_cast<const float4*>(G0 + (size_t)orow * n + 2 * c2));
+                }
+#pragma unroll
+                for (int u = 0; u < HALF; ++u) {
+                    const int e = t + NT * (h * HALF + u), row = e / HW, c2 = e % HW;
+                    const int orow = q * NPC + row / Q + L * (row % Q);
+                    const float4 cv = *reinterpret_cast<const float4*>(&buf[row * PM + 2 * c2]);
+                    __stcg(reinterpret_cast<float4*>(G0 + (size_t)orow * n + 2 * c2), f4add(gv[u], cv));
+                }
+            }
+        } else {
+            constexpr int PER = L * M / NT, HALF = PER / 2;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float2 gv[HALF];
+#pragma unroll
+                for (int u = 0; u < HALF; ++u) {
+                    const int e = t + NT * (h * HALF + u), row = e / M, c = e % M;
+                    const int orow = q * NPC + row / Q + L * (row % Q);
+                    gv[u] = __ldcg(G0 + (size_t)orow * n + c);
+                }
+#pragma unroll
+                for (int u = 0; u < HALF; ++u) {
+                    const int e = t + NT * (h * HALF + u), row = e / M, c = e % M;
+                    const int orow = q * NPC + row / Q + L * (row % Q);
+                    __stcg(G0 + (size_t)orow * n + c, cadd(gv[u], buf[row * PM + c]));
+                }
+            }
+        }
+        // (D) publish: this CTA's rows of frame k are final
+        __syncthreads();
+        if (t == 0) red_release_gpu_add(r.done + k, 1u);
+        ph ^= 1u;
+    }
+}
+
+// grad = -v (MG/OPT shift) or 0, <v,z> partial per block, counters zeroed
+template <typename C>
+__global__ void __launch_bounds__(256) k_rmw_init(const C* __restrict__ v, const C* __restrict__ z,
+                                                  C* __restrict__ grad, size_t len, double* dotp,
+                                                  unsigned* done, int N, unsigned* work) {
+    __shared__ double red[8];
+    const size_t chunk = (len + gridDim.x - 1) / gridDim.x;
+    const size_t lo = blockIdx.x * chunk, hi = min(lo + chunk, len);
+    double d = 0.0;
+    for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        C gv;
+        if (v) {
+            const C vv = v[i], zz = z[i];
+            gv.x = -vv.x;
+            gv.y = -vv.y;
+            d += (double)vv.x * (double)zz.x + (double)vv.y * (double)zz.y;
+        } else {
+            gv.x = 0;
+            gv.y = 0;
+        }
+        grad[i] = gv;
+    }
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (size_t)N; i += (size_t)gridDim.x * blockDim.x)
+        done[i] = 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *work = 0u;
+    if (!dotp) return;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = d;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < 8; ++i) s += red[i];
+        dotp[blockIdx.x] = s;
+    }
+}
+
+}  // namespace ptg

@@ -21,6 +21,7 @@
 #include <cudaTypedefs.h>
 
 #include "frame_cl.cuh"
+#include "frame_rmw.cuh"
 #include "frame_kernels.cuh"
 #include "frame_multipass.cuh"
 #include "frame_tma.cuh"
@@ -332,10 +333,9 @@ void launch_cl_ql(Plan& p, const FrameArgs<float>& a, int count, const float* ap
     else launch_cl_t<Q, L, OP, false>(p, a, count, ap, tw);
 }
 
-template <int OP>
-void launch_cl(Plan& p, const FrameArgs<float>& a, int count, const float* data) {
-    const float* ap = cl_amp(p, data);
-    if (!p.cl_tw.p) {   // W_M^i, i < M, in fp64 rounded once
+// W_M^i, i < M, in fp64 rounded once
+const float2* cl_twiddles(Plan& p) {
+    if (!p.cl_tw.p) {
         std::vector<float> h(2 * (size_t)p.M);
         for (int i = 0; i < p.M; ++i) {
             const double th = 2.0 * M_PI * i / p.M;
@@ -345,10 +345,58 @@ void launch_cl(Plan& p, const FrameArgs<float>& a, int count, const float* data)
         p.cl_tw.alloc(h.size() * sizeof(float));
         PTG_CUDA(cudaMemcpyAsync(p.cl_tw.p, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice, p.stream));
     }
-    const float2* tw = p.cl_tw.as<const float2>();
+    return p.cl_tw.as<const float2>();
+}
+
+template <int OP>
+void launch_cl(Plan& p, const FrameArgs<float>& a, int count, const float* data) {
+    const float* ap = cl_amp(p, data);
+    const float2* tw = cl_twiddles(p);
     const int L = cl_line(p);
     if (p.M == 128) L == 32 ? launch_cl_ql<4, 32, OP>(p, a, count, ap, tw) : launch_cl_ql<2, 64, OP>(p, a, count, ap, tw);
     else L == 32 ? launch_cl_ql<8, 32, OP>(p, a, count, ap, tw) : launch_cl_ql<4, 64, OP>(p, a, count, ap, tw);
+}
+
+// ------------------------------------------- persistent RMW frames (M = 128, 256)
+template <int Q, int L, int OP, bool PROBE>
+void launch_rmw_t(Plan& p, const FrameArgs<float>& a, const float* amp_perm, const float2* tw, float2* grad) {
+    constexpr size_t smem = cl_smem_bytes<Q, L>();
+    auto kern = frame_rmw_kernel<Q, L, OP, PROBE>;
+    set_smem_attr(kern, smem);
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(Q * L);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = p.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = Q;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (!p.rmw_clusters) {   // persistent grid: the clusters that fit at once
+        cfg.gridDim = dim3(Q);
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, (void*)kern, &cfg) != cudaSuccess || ncl < 1) {
+            cudaGetLastError();
+            ncl = 148 / Q;
+        }
+        p.rmw_clusters = ncl;
+    }
+    const int ncl = std::max(1, std::min(p.rmw_clusters, p.N));
+    cfg.gridDim = dim3((unsigned)ncl * Q);
+    RmwArgs r{p.rmw_order.as<const int>(), p.rmw_dep_off.as<const int>(), p.rmw_dep_idx.as<const int>(),
+              p.rmw_done.as<unsigned>(), p.rmw_work.as<unsigned>(), grad, p.N};
+    const float2* pe = PROBE ? probe_epi_table(p, OP) : nullptr;
+    PTG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, amp_perm, tw, pe, r));
+}
+
+template <int OP>
+void launch_rmw(Plan& p, const FrameArgs<float>& a, const float* data, float2* grad) {
+    const float* ap = cl_amp(p, data);
+    const float2* tw = cl_twiddles(p);
+    if (p.M == 128) a.probe ? launch_rmw_t<4, 32, OP, true>(p, a, ap, tw, grad) : launch_rmw_t<4, 32, OP, false>(p, a, ap, tw, grad);
+    else a.probe ? launch_rmw_t<8, 32, OP, true>(p, a, ap, tw, grad) : launch_rmw_t<8, 32, OP, false>(p, a, ap, tw, grad);
 }
 
 // objective frame kernel: TMA/register path for complex64 patch frames up to
@@ -882,6 +930,73 @@ bool choose_planes(Plan& p) {
     return true;
 }
 
+// ------------------------------------------------------- RMW order + deps
+// Summation / dispatch order of the RMW overlap-add (frame_rmw.cuh): positions
+// sorted by window row (stable: scan order within a row), cut into groups of
+// nearby rows (a new group once the row moved by >= w/8), each group greedily
+// coloured into pairwise non-overlapping classes and emitted class by class.
+// deps(k) = every earlier (in this order) frame whose window overlaps k's.
+// Deterministic for given positions.
+void build_rmw(Plan& p) {
+    const int N = p.N, w = p.w;
+    auto r0 = [&](int j) { return p.pos_h[2 * (size_t)j]; };
+    auto c0 = [&](int j) { return p.pos_h[2 * (size_t)j + 1]; };
+    auto overlap = [&](int a_, int b_) { return std::abs(r0(a_) - r0(b_)) < w && std::abs(c0(a_) - c0(b_)) < w; };
+    std::vector<int> idx(N);
+    for (int j = 0; j < N; ++j) idx[j] = j;
+    std::stable_sort(idx.begin(), idx.end(), [&](int a_, int b_) { return r0(a_) < r0(b_); });
+    std::vector<int> order;
+    order.reserve(N);
+    const int gap = std::max(1, w / 8);
+    for (int s = 0; s < N;) {
+        int e = s + 1;
+        while (e < N && r0(idx[e]) - r0(idx[s]) < gap) ++e;
+        std::vector<int> col(e - s, 0);
+        int ncol = 0;
+        for (int i = s; i < e; ++i) {
+            std::vector<char> used(ncol + 1, 0);
+            for (int i2 = s; i2 < i; ++i2)
+                if (overlap(idx[i], idx[i2])) used[col[i2 - s]] = 1;
+            int c = 0;
+            while (used[c]) ++c;
+            col[i - s] = c;
+            ncol = std::max(ncol, c + 1);
+        }
+        for (int c = 0; c < ncol; ++c)
+            for (int i = s; i < e; ++i)
+                if (col[i - s] == c) order.push_back(idx[i]);
+        s = e;
+    }
+    // dependencies through a grid of w x w cells
+    const int G = std::max(1, (p.n + w - 1) / w);
+    std::vector<std::vector<int>> cells((size_t)G * G);   // order indices
+    std::vector<int> off(N + 1, 0), dep;
+    dep.reserve((size_t)N * 32);
+    for (int k = 0; k < N; ++k) {
+        const int j = order[k];
+        const int cy = std::min(r0(j) / w, G - 1), cx = std::min(c0(j) / w, G - 1);
+        for (int yy = std::max(0, cy - 1); yy <= std::min(G - 1, cy + 1); ++yy)
+            for (int xx = std::max(0, cx - 1); xx <= std::min(G - 1, cx + 1); ++xx)
+                for (int k2 : cells[(size_t)yy * G + xx])
+                    if (overlap(j, order[k2])) dep.push_back(k2);
+        std::sort(dep.begin() + off[k], dep.end());
+        off[k + 1] = (int)dep.size();
+        cells[(size_t)cy * G + cx].push_back(k);
+    }
+    p.rmw_order_h = order;
+    p.rmw_order.alloc(std::max<size_t>(1, (size_t)N) * sizeof(int));
+    p.rmw_dep_off.alloc((size_t)(N + 1) * sizeof(int));
+    p.rmw_dep_idx.alloc(std::max<size_t>(1, dep.size()) * sizeof(int));
+    p.rmw_done.alloc(std::max<size_t>(1, (size_t)N) * sizeof(unsigned));
+    p.rmw_work.alloc(sizeof(unsigned));
+    if (N) PTG_CUDA(cudaMemcpyAsync(p.rmw_order.p, order.data(), (size_t)N * sizeof(int), cudaMemcpyHostToDevice, p.stream));
+    PTG_CUDA(cudaMemcpyAsync(p.rmw_dep_off.p, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice, p.stream));
+    if (!dep.empty())
+        PTG_CUDA(cudaMemcpyAsync(p.rmw_dep_idx.p, dep.data(), dep.size() * sizeof(int), cudaMemcpyHostToDevice, p.stream));
+    // the host vectors die with this scope: the copies must have been made
+    PTG_CUDA(cudaStreamSynchronize(p.stream));
+}
+
 // --------------------------------------------------------- chunks / tiles
 void build_chunks(Plan& p) {
     p.tiles_x = (p.n + kTileW - 1) / kTileW;
@@ -889,6 +1004,24 @@ void build_chunks(Plan& p) {
     p.mp = !frame_single_cta(p.prec, p.M);
     p.cl = cl_path_ok(p);
     p.planes_mode = choose_planes(p);
+    // RMW overlap-add for the cluster path when the planes do not fit
+    // (PTG_NO_RMW=1 selects the stash + gather path instead; read per plan)
+    const bool no_rmw = getenv("PTG_NO_RMW") && getenv("PTG_NO_RMW")[0] == '1';
+    p.rmw_mode = !p.planes_mode && p.cl && p.w == p.M && p.N > 0 && !no_rmw;
+    if (p.rmw_mode) {   // one chunk, no tile lists, no stash
+        auto c = std::make_unique<Chunk>();
+        c->first = 0;
+        c->count = p.N;
+        p.chunk_size = p.N;
+        p.chunks.clear();
+        p.chunks.push_back(std::move(c));
+        p.stash.alloc(p.celem());
+        p.misfit_per_pos = p.M / 32;
+        p.misfit.alloc((size_t)p.N * p.misfit_per_pos * sizeof(double));
+        p.dotp.alloc((size_t)kRmwInitBlocks * sizeof(double));
+        build_rmw(p);
+        return;
+    }
     if (p.planes_mode) {   // one chunk, no tile lists, no stash
         auto c = std::make_unique<Chunk>();
         c->first = 0;
@@ -1201,6 +1334,31 @@ template <typename T>
 static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad, double* value_dev) {
     using C = cplx<T>;
     const T* data = metric == PTG_DISTANCE ? p.amp.as<const T>() : p.inten.as<const T>();
+    if constexpr (sizeof(T) == 4) {
+        if (p.rmw_mode) {
+            // init (grad = -v | 0, <v,z> partials, counters) -> persistent RMW
+            // frames -> value; all on the plan's stream
+            p.ev_begin(1);
+            k_rmw_init<C><<<kRmwInitBlocks, 256, 0, p.stream>>>(static_cast<const C*>(v), static_cast<const C*>(z),
+                                                                static_cast<C*>(grad), p.nn(),
+                                                                v ? p.dotp.as<double>() : nullptr,
+                                                                p.rmw_done.as<unsigned>(), p.N, p.rmw_work.as<unsigned>());
+            PTG_CHECK_LAUNCH();
+            p.ev_end();
+            ++p.launches;
+            FrameArgs<T> a = frame_args<T>(p, z, data);
+            p.ev_begin(0);
+            if (metric == PTG_DISTANCE) launch_rmw<OP_DISTANCE>(p, a, data, static_cast<float2*>(grad));
+            else launch_rmw<OP_INTENSITY>(p, a, data, static_cast<float2*>(grad));
+            p.ev_end();
+            ++p.launches;
+            k_finalize<<<1, 256, 0, p.stream>>>(p.misfit.as<const double>(), p.N * p.misfit_per_pos,
+                                                p.dotp.as<const double>(), v ? kRmwInitBlocks : 0, value_dev);
+            PTG_CHECK_LAUNCH();
+            ++p.launches;
+            return;
+        }
+    }
     const bool single = p.chunks.size() == 1;
     // fused last-block finalize in the gather (single-chunk plans); PTG_NOFUSE=1
     // selects the separate finalize kernel (kept for A/B measurement)

@@ -65,7 +65,8 @@ struct Chunk {
 
 constexpr int kTileW = 64;   // overlap-add gather tile: 64 x 8 pixels, 2 per thread (32 x 8 block)
 constexpr int kTileH = 8;
-constexpr int kHvalDoubles = 16;   // pinned host scalars per plan (never reallocated)
+constexpr int kHvalDoubles = 16;
+constexpr int kRmwInitBlocks = 1024;   // fixed grid of k_rmw_init => fixed <v,z> partition   // pinned host scalars per plan (never reallocated)
 
 struct Plan {
     int n = 0, M = 0, w = 0, N = 0, prec = PTG_C64, device = 0;
@@ -139,6 +140,14 @@ struct Plan {
     int amp_cl_line = 0;
     uint64_t amp_cl_gen = ~0ull;
     uint64_t data_gen = 0;   // bumped whenever amp / inten are rewritten
+
+    // RMW overlap-add (frame_rmw.cuh): persistent cluster kernel adding each
+    // frame's contribution straight into the gradient in a fixed,
+    // dependency-ordered sequence (no stash, no gather)
+    bool rmw_mode = false;
+    int rmw_clusters = 0;            // persistent grid (co-resident clusters)
+    DevMem rmw_order, rmw_dep_off, rmw_dep_idx, rmw_done, rmw_work;
+    std::vector<int> rmw_order_h;    // for tests / diagnostics
 
     // multi-pass path for frames larger than one CTA (frame_multipass.cuh)
     bool mp = false;

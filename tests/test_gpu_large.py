@@ -95,6 +95,7 @@ def test_multichunk_stash_matches_single(oracle, monkeypatch, budget_mb):
     cfg = synth.CONFIGS[3]
     prob, z, v, data, probe, pos, n = _case(oracle, cfg)
     monkeypatch.setenv("PTG_NO_PLANES", "1")
+    monkeypatch.setenv("PTG_NO_RMW", "1")
     monkeypatch.setenv("PTG_STASH_BUDGET_MB", str(budget_mb))
     plan = Plan(n, cfg.M, cfg.w, pos, data, probe, precision="c64")
     _check(plan, prob, oracle, z, v)
@@ -155,3 +156,49 @@ def test_config5_full_properties():
     assert float(torch.linalg.vector_norm(gv - (grads[0] - v)) / torch.linalg.vector_norm(gv)) <= 1e-6
     for p in plans:
         p.close()
+
+
+# ------------------------------------------------ RMW overlap-add (frame_rmw.cuh)
+@pytest.mark.parametrize("M,steps,step,jitter,metric", [(128, 6, 40, 0, 0), (128, 7, 24, 2, 0), (256, 4, 48, 0, 0),
+                                                        (256, 5, 64, 3, 0), (256, 4, 48, 0, 1)])
+def test_rmw_matches_oracle(oracle, monkeypatch, M, steps, step, jitter, metric):
+    """The persistent dependency-ordered RMW path (forced for small problems
+    with PTG_NO_PLANES=1): odd window columns (jitter), both metrics, shift."""
+    from paper_1810_05628_b200 import Plan, synth
+    n = (steps - 1) * step + M + 2 * jitter + 6
+    cfg = synth.Config(0, n, M, steps, step, 6.0, M / 4, 0.001, "c64", jitter=jitter)
+    obj, probe, pos = synth.make_inputs(cfg)
+    probe, obj = _r64(probe), _r64(obj)
+    data = oracle.simulate(n, M, M, pos, obj, probe).astype(np.float32)
+    z = _r64(obj * 0.9 + 0.05 * rand_field(n, 7))
+    v = _r64(0.01 * rand_field(n, 8))
+    prob = oracle.Problem(n, M, M, pos, data.astype(np.float64), probe, metric)
+    monkeypatch.setenv("PTG_NO_PLANES", "1")
+    plan = Plan(n, M, M, pos, data, probe, precision="c64")
+    for vv in (v, None):
+        gv, gg = plan.evaluate(z, vv, metric=metric)
+        wv, wg = oracle.evaluate(prob, z, vv)
+        assert rel(gv, wv) <= C64_VAL, (gv, wv)
+        assert rel_l2(gg, wg) <= C64_GRAD, rel_l2(gg, wg)
+    # bitwise reproducible run to run (fixed dependency-ordered summation)
+    g1 = plan.evaluate(z, v, metric=metric)
+    g2 = plan.evaluate(z, v, metric=metric)
+    assert g1[0] == g2[0] and np.array_equal(g1[1], g2[1])
+    plan.close()
+
+
+def test_rmw_matches_stash_path(oracle, monkeypatch):
+    """Config-3 geometry: RMW and stash + gather agree (different summation
+    orders of the same contributions)."""
+    from paper_1810_05628_b200 import Plan, synth
+    cfg = synth.CONFIGS[3]
+    prob, z, v, data, probe, pos, n = _case(oracle, cfg)
+    monkeypatch.setenv("PTG_NO_PLANES", "1")
+    a = Plan(n, cfg.M, cfg.w, pos, data, probe, precision="c64")
+    monkeypatch.setenv("PTG_NO_RMW", "1")
+    b = Plan(n, cfg.M, cfg.w, pos, data, probe, precision="c64")
+    va, ga = a.evaluate(z, v)
+    vb, gb = b.evaluate(z, v)
+    assert rel(va, vb) <= 1e-6 and rel_l2(ga, gb) <= 1e-5
+    a.close()
+    b.close()
