@@ -997,6 +997,15 @@ void build_rmw(Plan& p) {
     PTG_CUDA(cudaStreamSynchronize(p.stream));
 }
 
+// whole-frame scratch of the multi-pass kernels (simulate / project / c128
+// objective at large M): ~64 MiB, stays L2-resident between passes
+void build_mp_scratch(Plan& p) {
+    if (!p.mp) return;
+    const size_t fb = p.MM() * p.celem();
+    p.mp_chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(p.N, 1), ((size_t)64 << 20) / fb));
+    p.mp_scratch.alloc((size_t)p.mp_chunk * fb);
+}
+
 // --------------------------------------------------------- chunks / tiles
 void build_chunks(Plan& p) {
     p.tiles_x = (p.n + kTileW - 1) / kTileW;
@@ -1019,6 +1028,7 @@ void build_chunks(Plan& p) {
         p.misfit_per_pos = p.M / 32;
         p.misfit.alloc((size_t)p.N * p.misfit_per_pos * sizeof(double));
         p.dotp.alloc((size_t)kRmwInitBlocks * sizeof(double));
+        build_mp_scratch(p);
         build_rmw(p);
         return;
     }
@@ -1095,11 +1105,7 @@ void build_chunks(Plan& p) {
     }
     p.stash.alloc(std::max<size_t>(1, (size_t)cs * p.w * stash_pitch(p.w)) * p.celem());
     p.misfit_per_pos = p.cl ? p.M / 32 : p.mp ? p.M / kMpLines : 1;
-    if (p.mp) {   // ~64 MiB of whole-frame scratch: stays L2-resident between passes
-        const size_t fb = p.MM() * p.celem();
-        p.mp_chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(p.N, 1), ((size_t)64 << 20) / fb));
-        p.mp_scratch.alloc((size_t)p.mp_chunk * fb);
-    }
+    build_mp_scratch(p);
     p.misfit.alloc(std::max<size_t>(1, (size_t)p.N * p.misfit_per_pos) * sizeof(double));
     // dot partials: one per tile (single chunk) or one per k_shift block
     p.dotp.alloc(std::max<size_t>((size_t)ntiles, 1024) * sizeof(double));
