@@ -281,6 +281,10 @@ int cl_line(const Plan& p) {
     static const int env = getenv("PTG_CL_L") ? atoi(getenv("PTG_CL_L")) : 0;
     return env == 64 ? 64 : 32;
 }
+// local line of the persistent RMW kernel (fixed per plan at creation):
+// M = 256 -> 16 (16-CTA clusters, 4 CTAs per SM) unless PTG_RMW_L=32
+// (8-CTA clusters, 2 per SM); M = 128 -> 32
+int rmw_line(const Plan& p) { return p.M == 256 ? p.rmw_line : 32; }
 
 template <int Q, int L>
 void perm_amp(Plan& p, const float* data, size_t total) {
@@ -292,12 +296,12 @@ void perm_amp(Plan& p, const float* data, size_t total) {
 
 // amplitudes (or intensities) permuted for frame_cl_kernel, rebuilt when the
 // source buffer, its contents (data_gen) or the split change
-const float* cl_amp(Plan& p, const float* data) {
-    const int L = cl_line(p);
+const float* cl_amp(Plan& p, const float* data, int L) {
     if (p.amp_cl_src != data || p.amp_cl_gen != p.data_gen || p.amp_cl_line != L) {
         const size_t total = (size_t)p.N * p.MM();
         p.amp_cl.ensure(total * sizeof(float));
         if (p.M == 128) L == 32 ? perm_amp<4, 32>(p, data, total) : perm_amp<2, 64>(p, data, total);
+        else if (L == 16) perm_amp<16, 16>(p, data, total);
         else L == 32 ? perm_amp<8, 32>(p, data, total) : perm_amp<4, 64>(p, data, total);
         p.amp_cl_src = data;
         p.amp_cl_gen = p.data_gen;
@@ -350,7 +354,7 @@ const float2* cl_twiddles(Plan& p) {
 
 template <int OP>
 void launch_cl(Plan& p, const FrameArgs<float>& a, int count, const float* data) {
-    const float* ap = cl_amp(p, data);
+    const float* ap = cl_amp(p, data, cl_line(p));
     const float2* tw = cl_twiddles(p);
     const int L = cl_line(p);
     if (p.M == 128) L == 32 ? launch_cl_ql<4, 32, OP>(p, a, count, ap, tw) : launch_cl_ql<2, 64, OP>(p, a, count, ap, tw);
@@ -363,6 +367,13 @@ void launch_rmw_t(Plan& p, const FrameArgs<float>& a, const float* amp_perm, con
     constexpr size_t smem = cl_smem_bytes<Q, L>();
     auto kern = frame_rmw_kernel<Q, L, OP, PROBE>;
     set_smem_attr(kern, smem);
+    if constexpr (Q > 8) {   // 16-CTA clusters are opt-in (non-portable)
+        static bool attr[64] = {};
+        if (!attr[p.device]) {
+            PTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            attr[p.device] = true;
+        }
+    }
     cudaLaunchConfig_t cfg{};
     cfg.blockDim = dim3(Q * L);
     cfg.dynamicSmemBytes = smem;
@@ -393,9 +404,10 @@ void launch_rmw_t(Plan& p, const FrameArgs<float>& a, const float* amp_perm, con
 
 template <int OP>
 void launch_rmw(Plan& p, const FrameArgs<float>& a, const float* data, float2* grad) {
-    const float* ap = cl_amp(p, data);
+    const float* ap = cl_amp(p, data, rmw_line(p));
     const float2* tw = cl_twiddles(p);
     if (p.M == 128) a.probe ? launch_rmw_t<4, 32, OP, true>(p, a, ap, tw, grad) : launch_rmw_t<4, 32, OP, false>(p, a, ap, tw, grad);
+    else if (rmw_line(p) == 16) a.probe ? launch_rmw_t<16, 16, OP, true>(p, a, ap, tw, grad) : launch_rmw_t<16, 16, OP, false>(p, a, ap, tw, grad);
     else a.probe ? launch_rmw_t<8, 32, OP, true>(p, a, ap, tw, grad) : launch_rmw_t<8, 32, OP, false>(p, a, ap, tw, grad);
 }
 
@@ -1025,7 +1037,11 @@ void build_chunks(Plan& p) {
         p.chunks.clear();
         p.chunks.push_back(std::move(c));
         p.stash.alloc(p.celem());
-        p.misfit_per_pos = p.M / 32;
+        {
+            const char* e = getenv("PTG_RMW_L");
+            p.rmw_line = (e && atoi(e) == 32) ? 32 : 16;
+        }
+        p.misfit_per_pos = cl_mpp(p.M / rmw_line(p), p.M);
         p.misfit.alloc((size_t)p.N * p.misfit_per_pos * sizeof(double));
         p.dotp.alloc((size_t)kRmwInitBlocks * sizeof(double));
         build_mp_scratch(p);

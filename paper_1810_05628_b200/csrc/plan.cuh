@@ -146,6 +146,7 @@ struct Plan {
     // dependency-ordered sequence (no stash, no gather)
     bool rmw_mode = false;
     int rmw_clusters = 0;            // persistent grid (co-resident clusters)
+    int rmw_line = 16;               // local line L of the M = 256 variant (Q = 256 / L CTAs per cluster)
     DevMem rmw_order, rmw_dep_off, rmw_dep_idx, rmw_done, rmw_work;
     std::vector<int> rmw_order_h;    // for tests / diagnostics
 

@@ -131,6 +131,7 @@ def test_config5_full_properties():
     plans = []
     for sel in (pos, rows[0::2].reshape(-1, 2), rows[1::2].reshape(-1, 2)):
         p = Plan(cfg.n, cfg.M, cfg.w, sel, None, probe, precision="c64")
+        p.set_stream(torch.cuda.current_stream().cuda_stream)   # ordered after torch's writes of z / v
         p.simulate(obj, copy_out=False)
         plans.append(p)
     g = torch.Generator(device="cpu").manual_seed(3)
