@@ -51,11 +51,8 @@ __host__ __device__ constexpr size_t cl_smem_bytes() {
     return sizeof(float2) * ((size_t)L * cl_pitch<Q, L>() + (size_t)Q * L)     // L rows + twiddle table
            + (cl_amp_staged<Q, L>() ? sizeof(float) * (size_t)L * cl_amp_pitch<Q, L>() : 0);
 }
-#ifndef PTG_RMW16_BLOCKS
-#define PTG_RMW16_BLOCKS 3   // CTAs per SM of the 16-CTA-cluster variant (L = 16)
-#endif
 template <int Q, int L>
-__host__ __device__ constexpr int cl_min_blocks() { return L == 16 ? PTG_RMW16_BLOCKS : L == 32 ? (Q == 4 ? 4 : 2) : Q == 2 ? 2 : 1; }
+__host__ __device__ constexpr int cl_min_blocks() { return L == 32 ? (Q == 4 ? 4 : 2) : Q == 2 ? 2 : 1; }
 // per-position misfit slots written by a cluster variant (one per CTA, at least M / 32)
 __host__ __device__ constexpr int cl_mpp(int Q, int M) { return Q > M / 32 ? Q : M / 32; }
 
@@ -80,8 +77,7 @@ template <int Q>
 __device__ __forceinline__ void dft_q(float2* v) {
     if constexpr (Q == 2) dft2<false>(v[0], v[1]);
     else if constexpr (Q == 4) dft4<false>(v[0], v[1], v[2], v[3]);
-    else if constexpr (Q == 8) dft8<false>(v);
-    else dft16<false>(v);
+    else dft8<false>(v);
 }
 
 template <int Q, int L, int OP, bool PROBE>

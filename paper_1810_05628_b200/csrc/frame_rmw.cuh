@@ -45,7 +45,7 @@ struct RmwArgs {
     unsigned* done;       // [N] per order index: CTAs finished (Q = complete), zeroed per evaluation
     unsigned* work;       // dispatch counter, zeroed per evaluation
     float2* grad;         // gradient, row pitch a.n
-    int N;
+    int kbeg, kend;       // this launch's frames: order indices [kbeg, kend) (earlier ones are complete)
 };
 
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
@@ -114,8 +114,8 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         }
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-        const int k = s_item;
-        if (k >= r.N) break;
+        const int k = r.kbeg + s_item;
+        if (k >= r.kend) break;
         const int j = __ldg(r.order + k);
         const int2 pj = a.pos[j];
 
@@ -129,31 +129,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
 
         // gather fused with the column DIF butterflies (frame_cl.cuh)
         float2 x[L];
-        if constexpr (Q >= 16) {
-            // one butterfly row per CTA (NPC = 1): its Q object values first,
-            // the probe multiplied in as its values arrive (register budget)
-            // rows q + L s: one running pointer each (64-bit addresses for
-            // every row would not fit the register budget next to the values)
-            const float2* zc = a.z + (size_t)(pj.x + q) * n + pj.y + t;
-            const size_t zstep = (size_t)L * n;
-            float2 v[Q];
-#pragma unroll
-            for (int s = 0; s < Q; ++s) {
-                v[s] = ldg_pinned(zc);
-                zc += zstep;
-            }
-            if constexpr (PROBE) {
-                const float2* pc = a.probe + (size_t)q * M + t;
-#pragma unroll
-                for (int s = 0; s < Q; ++s) v[s] = cmul(ldg_pinned(pc + (size_t)s * L * M), v[s]);
-            }
-            dft_q<Q>(v);
-#pragma unroll
-            for (int s = 1; s < Q; ++s) v[s] = cmul(tw[q * s], v[s]);
-#pragma unroll
-            for (int s = 0; s < Q; ++s)
-                st_async_f2(mapa_u32(smem_u32(buf + q * PM + t), s), v[s], mapa_u32(bar_g_u, s));
-        } else {
+        {
             constexpr int BT = 16 / Q;
             const float2* zc = a.z + (size_t)pj.x * n + pj.y + t;
 #pragma unroll 1

@@ -281,10 +281,11 @@ int cl_line(const Plan& p) {
     static const int env = getenv("PTG_CL_L") ? atoi(getenv("PTG_CL_L")) : 0;
     return env == 64 ? 64 : 32;
 }
-// local line of the persistent RMW kernel (fixed per plan at creation):
-// M = 256 -> 16 (16-CTA clusters, 4 CTAs per SM) unless PTG_RMW_L=32
-// (8-CTA clusters, 2 per SM); M = 128 -> 32
-int rmw_line(const Plan& p) { return p.M == 256 ? p.rmw_line : 32; }
+// local line of the persistent RMW kernel: 8-CTA (M = 256) / 4-CTA (M = 128)
+// clusters of 32-row CTAs.  Measured and rejected: 16-CTA clusters of 16-row
+// CTAs at 3 per SM (M = 256): 27.9 vs 22.5 ms per config-5 evaluation (more
+// cluster-barrier and membar stalls, 25 % more instructions)
+int rmw_line(const Plan&) { return 32; }
 
 template <int Q, int L>
 void perm_amp(Plan& p, const float* data, size_t total) {
@@ -301,7 +302,6 @@ const float* cl_amp(Plan& p, const float* data, int L) {
         const size_t total = (size_t)p.N * p.MM();
         p.amp_cl.ensure(total * sizeof(float));
         if (p.M == 128) L == 32 ? perm_amp<4, 32>(p, data, total) : perm_amp<2, 64>(p, data, total);
-        else if (L == 16) perm_amp<16, 16>(p, data, total);
         else L == 32 ? perm_amp<8, 32>(p, data, total) : perm_amp<4, 64>(p, data, total);
         p.amp_cl_src = data;
         p.amp_cl_gen = p.data_gen;
@@ -363,17 +363,11 @@ void launch_cl(Plan& p, const FrameArgs<float>& a, int count, const float* data)
 
 // ------------------------------------------- persistent RMW frames (M = 128, 256)
 template <int Q, int L, int OP, bool PROBE>
-void launch_rmw_t(Plan& p, const FrameArgs<float>& a, const float* amp_perm, const float2* tw, float2* grad) {
+void launch_rmw_t(Plan& p, const FrameArgs<float>& a, const float* amp_perm, const float2* tw, float2* grad,
+                  int kbeg, int kend) {
     constexpr size_t smem = cl_smem_bytes<Q, L>();
     auto kern = frame_rmw_kernel<Q, L, OP, PROBE>;
     set_smem_attr(kern, smem);
-    if constexpr (Q > 8) {   // 16-CTA clusters are opt-in (non-portable)
-        static bool attr[64] = {};
-        if (!attr[p.device]) {
-            PTG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            attr[p.device] = true;
-        }
-    }
     cudaLaunchConfig_t cfg{};
     cfg.blockDim = dim3(Q * L);
     cfg.dynamicSmemBytes = smem;
@@ -394,21 +388,25 @@ void launch_rmw_t(Plan& p, const FrameArgs<float>& a, const float* amp_perm, con
         }
         p.rmw_clusters = ncl;
     }
-    const int ncl = std::max(1, std::min(p.rmw_clusters, p.N));
+    const int ncl = std::max(1, std::min(p.rmw_clusters, kend - kbeg));
     cfg.gridDim = dim3((unsigned)ncl * Q);
     RmwArgs r{p.rmw_order.as<const int>(), p.rmw_dep_off.as<const int>(), p.rmw_dep_idx.as<const int>(),
-              p.rmw_done.as<unsigned>(), p.rmw_work.as<unsigned>(), grad, p.N};
+              p.rmw_done.as<unsigned>(), p.rmw_work.as<unsigned>(), grad, kbeg, kend};
     const float2* pe = PROBE ? probe_epi_table(p, OP) : nullptr;
     PTG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, amp_perm, tw, pe, r));
 }
 
+// frames [kbeg, kend) of the RMW order; the dispatch counter must be zero
 template <int OP>
-void launch_rmw(Plan& p, const FrameArgs<float>& a, const float* data, float2* grad) {
+void launch_rmw(Plan& p, const FrameArgs<float>& a, const float* data, float2* grad, int kbeg, int kend) {
     const float* ap = cl_amp(p, data, rmw_line(p));
     const float2* tw = cl_twiddles(p);
-    if (p.M == 128) a.probe ? launch_rmw_t<4, 32, OP, true>(p, a, ap, tw, grad) : launch_rmw_t<4, 32, OP, false>(p, a, ap, tw, grad);
-    else if (rmw_line(p) == 16) a.probe ? launch_rmw_t<16, 16, OP, true>(p, a, ap, tw, grad) : launch_rmw_t<16, 16, OP, false>(p, a, ap, tw, grad);
-    else a.probe ? launch_rmw_t<8, 32, OP, true>(p, a, ap, tw, grad) : launch_rmw_t<8, 32, OP, false>(p, a, ap, tw, grad);
+    if (p.M == 128)
+        a.probe ? launch_rmw_t<4, 32, OP, true>(p, a, ap, tw, grad, kbeg, kend)
+                : launch_rmw_t<4, 32, OP, false>(p, a, ap, tw, grad, kbeg, kend);
+    else
+        a.probe ? launch_rmw_t<8, 32, OP, true>(p, a, ap, tw, grad, kbeg, kend)
+                : launch_rmw_t<8, 32, OP, false>(p, a, ap, tw, grad, kbeg, kend);
 }
 
 // objective frame kernel: TMA/register path for complex64 patch frames up to
@@ -959,6 +957,8 @@ void build_rmw(Plan& p) {
     std::stable_sort(idx.begin(), idx.end(), [&](int a_, int b_) { return r0(a_) < r0(b_); });
     std::vector<int> order;
     order.reserve(N);
+    p.rmw_group_end.clear();
+    p.rmw_group_maxr0.clear();
     const int gap = std::max(1, w / 8);
     for (int s = 0; s < N;) {
         int e = s + 1;
@@ -977,8 +977,12 @@ void build_rmw(Plan& p) {
         for (int c = 0; c < ncol; ++c)
             for (int i = s; i < e; ++i)
                 if (col[i - s] == c) order.push_back(idx[i]);
+        p.rmw_group_end.push_back((int)order.size());
+        p.rmw_group_maxr0.push_back(r0(idx[e - 1]));
         s = e;
     }
+    p.rmw_sufmin_r0.assign(N + 1, p.n);
+    for (int k = N - 1; k >= 0; --k) p.rmw_sufmin_r0[k] = std::min(p.rmw_sufmin_r0[k + 1], r0(order[k]));
     // dependencies through a grid of w x w cells
     const int G = std::max(1, (p.n + w - 1) / w);
     std::vector<std::vector<int>> cells((size_t)G * G);   // order indices
@@ -1037,10 +1041,6 @@ void build_chunks(Plan& p) {
         p.chunks.clear();
         p.chunks.push_back(std::move(c));
         p.stash.alloc(p.celem());
-        {
-            const char* e = getenv("PTG_RMW_L");
-            p.rmw_line = (e && atoi(e) == 32) ? 32 : 16;
-        }
         p.misfit_per_pos = cl_mpp(p.M / rmw_line(p), p.M);
         p.misfit.alloc((size_t)p.N * p.misfit_per_pos * sizeof(double));
         p.dotp.alloc((size_t)kRmwInitBlocks * sizeof(double));
@@ -1370,8 +1370,8 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
             ++p.launches;
             FrameArgs<T> a = frame_args<T>(p, z, data);
             p.ev_begin(0);
-            if (metric == PTG_DISTANCE) launch_rmw<OP_DISTANCE>(p, a, data, static_cast<float2*>(grad));
-            else launch_rmw<OP_INTENSITY>(p, a, data, static_cast<float2*>(grad));
+            if (metric == PTG_DISTANCE) launch_rmw<OP_DISTANCE>(p, a, data, static_cast<float2*>(grad), 0, p.N);
+            else launch_rmw<OP_INTENSITY>(p, a, data, static_cast<float2*>(grad), 0, p.N);
             p.ev_end();
             ++p.launches;
             k_finalize<<<1, 256, 0, p.stream>>>(p.misfit.as<const double>(), p.N * p.misfit_per_pos,
@@ -1628,6 +1628,104 @@ static void eval_host_banded(Plan& p, int metric, const double* z, const double*
     if (value) *value = *p.hval.as<double>();
 }
 
+// ------------------------------------------------- banded host eval (RMW)
+// ptg_eval with host complex128 buffers on an RMW plan (configs 4-5): the
+// object goes up in K row bands over two copy engines; the frames whose
+// windows lie inside the rows uploaded so far run as one persistent RMW launch
+// per band (launches are stream-ordered, so every earlier frame is complete
+// when the next band's frames start -- the same summation order, bitwise the
+// same gradient as plan_eval); gradient rows no pending frame touches go back
+// (complex128) over the copy-out streams while later bands compute.  PCIe in,
+// compute and PCIe out overlap instead of adding up.
+static void eval_host_rmw(Plan& p, int metric, const double* z, double* value, double* grad) {
+    using C = float2;
+    const int n = p.n, w = p.w, N = p.N;
+    const size_t nn = p.nn();
+    const char* eb = getenv("PTG_RMW_BANDS");
+    const int K = eb ? std::max(1, std::min(64, atoi(eb))) : 8;
+    const int H = (n + K - 1) / K;
+    if (!p.s_in) {
+        PTG_CUDA(cudaStreamCreateWithFlags(&p.s_in, cudaStreamNonBlocking));
+        PTG_CUDA(cudaStreamCreateWithFlags(&p.s_out, cudaStreamNonBlocking));
+        PTG_CUDA(cudaStreamCreateWithFlags(&p.s_in2, cudaStreamNonBlocking));
+        PTG_CUDA(cudaStreamCreateWithFlags(&p.s_out2, cudaStreamNonBlocking));
+    }
+    const cudaStream_t sin[2] = {p.s_in, p.s_in2}, sout[2] = {p.s_out, p.s_out2};
+    while (p.ev_band.size() < (size_t)(2 * K + 4)) {
+        cudaEvent_t e;
+        PTG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        p.ev_band.push_back(e);
+    }
+    cudaEvent_t* ev_in = p.ev_band.data();
+    cudaEvent_t* ev_out = p.ev_band.data() + K;
+    cudaEvent_t ev_start = p.ev_band[2 * K], ev_val = p.ev_band[2 * K + 1];
+    p.zbuf.ensure(nn * sizeof(C));
+    p.gbuf.ensure(nn * sizeof(C));
+    p.stage.ensure(nn * 16);
+    p.stage_out.ensure(nn * 16);
+    double* st_z = p.stage.as<double>();
+    C* zd = p.zbuf.as<C>();
+    C* gd = p.gbuf.as<C>();
+    const float* data = metric == PTG_DISTANCE ? p.amp.as<const float>() : p.inten.as<const float>();
+    PTG_CUDA(cudaEventRecord(ev_start, p.stream));
+    for (int i = 0; i < 2; ++i) {
+        PTG_CUDA(cudaStreamWaitEvent(sin[i], ev_start, 0));
+        PTG_CUDA(cudaStreamWaitEvent(sout[i], ev_start, 0));
+    }
+    for (int b = 0; b < K; ++b) {
+        const size_t r0 = (size_t)std::min(n, b * H), r1 = (size_t)std::min(n, (b + 1) * H);
+        if (r1 > r0)
+            PTG_CUDA(cudaMemcpyAsync(st_z + 2 * r0 * n, z + 2 * r0 * n, (r1 - r0) * n * 16, cudaMemcpyHostToDevice,
+                                     sin[b & 1]));
+        PTG_CUDA(cudaEventRecord(ev_in[b], sin[b & 1]));
+    }
+    // gradient = 0, completion counters zeroed (no shift on this path)
+    k_rmw_init<C><<<kRmwInitBlocks, 256, 0, p.stream>>>(nullptr, nullptr, gd, nn, nullptr, p.rmw_done.as<unsigned>(), N,
+                                                        p.rmw_work.as<unsigned>());
+    PTG_CHECK_LAUNCH();
+    ++p.launches;
+    FrameArgs<float> a = frame_args<float>(p, zd, data);
+    int k_cur = 0;
+    size_t g = 0;        // row groups launched
+    size_t rows_out = 0;
+    for (int b = 0; b < K; ++b) {
+        const int r0 = std::min(n, b * H), r1 = std::min(n, (b + 1) * H);
+        PTG_CUDA(cudaStreamWaitEvent(p.stream, ev_in[b], 0));
+        if (r1 > r0) dev_from_c128(PTG_C64, zd + (size_t)r0 * n, st_z + 2 * (size_t)r0 * n, (size_t)(r1 - r0) * n, p.stream);
+        // whole row groups whose windows lie in the uploaded rows
+        while (g < p.rmw_group_end.size() && (b == K - 1 || p.rmw_group_maxr0[g] + w <= r1)) ++g;
+        const int k_end = g ? p.rmw_group_end[g - 1] : 0;
+        if (k_end > k_cur) {
+            PTG_CUDA(cudaMemsetAsync(p.rmw_work.p, 0, sizeof(unsigned), p.stream));
+            if (metric == PTG_DISTANCE) launch_rmw<OP_DISTANCE>(p, a, data, gd, k_cur, k_end);
+            else launch_rmw<OP_INTENSITY>(p, a, data, gd, k_cur, k_end);
+            ++p.launches;
+            k_cur = k_end;
+        }
+        // rows no pending frame touches are final
+        const size_t ready = b == K - 1 ? (size_t)n : (size_t)std::min(p.rmw_sufmin_r0[k_cur], r1);
+        if (ready > rows_out) {
+            const size_t o = rows_out * n, c = (ready - rows_out) * n;
+            dev_to_c128(PTG_C64, p.stage_out.as<double>() + 2 * o, gd + o, c, p.stream);
+            PTG_CUDA(cudaEventRecord(ev_out[b], p.stream));
+            PTG_CUDA(cudaStreamWaitEvent(sout[b & 1], ev_out[b], 0));
+            PTG_CUDA(cudaMemcpyAsync(grad + 2 * o, p.stage_out.as<double>() + 2 * o, c * 16, cudaMemcpyDeviceToHost,
+                                     sout[b & 1]));
+            rows_out = ready;
+        }
+    }
+    k_finalize<<<1, 256, 0, p.stream>>>(p.misfit.as<const double>(), N * p.misfit_per_pos, p.dotp.as<const double>(), 0,
+                                        p.value.as<double>());
+    PTG_CHECK_LAUNCH();
+    ++p.launches;
+    PTG_CUDA(cudaEventRecord(ev_val, p.stream));
+    PTG_CUDA(cudaStreamWaitEvent(p.s_out, ev_val, 0));
+    PTG_CUDA(cudaMemcpyAsync(p.hval.p, p.value.p, sizeof(double), cudaMemcpyDeviceToHost, p.s_out));
+    PTG_CUDA(cudaStreamSynchronize(p.s_out2));
+    PTG_CUDA(cudaStreamSynchronize(p.s_out));
+    if (value) *value = *p.hval.as<double>();
+}
+
 static bool host_pinned(const void* ptr) {
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
@@ -1640,6 +1738,10 @@ static bool host_pinned(const void* ptr) {
 void plan_eval_host(Plan& p, int metric, const double* z, const double* v, double* value, double* grad) {
     LaunchScope ls(p);
     plan_ensure(p, metric);
+    if (p.rmw_mode && !v && grad && !p.timing && !(getenv("PTG_NO_BANDED") && getenv("PTG_NO_BANDED")[0] == '1')) {
+        eval_host_rmw(p, metric, z, value, grad);
+        return;
+    }
     static const bool off = getenv("PTG_NO_BANDED") && getenv("PTG_NO_BANDED")[0] == '1';   // A/B switch
     bool sorted = true;
     for (int j = 1; j < p.N && sorted; ++j) sorted = p.pos_h[2 * j] >= p.pos_h[2 * (j - 1)];

@@ -146,9 +146,11 @@ struct Plan {
     // dependency-ordered sequence (no stash, no gather)
     bool rmw_mode = false;
     int rmw_clusters = 0;            // persistent grid (co-resident clusters)
-    int rmw_line = 16;               // local line L of the M = 256 variant (Q = 256 / L CTAs per cluster)
     DevMem rmw_order, rmw_dep_off, rmw_dep_idx, rmw_done, rmw_work;
     std::vector<int> rmw_order_h;    // for tests / diagnostics
+    // row groups of the order (ascending window rows): end index and largest
+    // window row of each; suffix minimum of the window rows (banded host eval)
+    std::vector<int> rmw_group_end, rmw_group_maxr0, rmw_sufmin_r0;
 
     // multi-pass path for frames larger than one CTA (frame_multipass.cuh)
     bool mp = false;

@@ -131,7 +131,6 @@ def test_config5_full_properties():
     plans = []
     for sel in (pos, rows[0::2].reshape(-1, 2), rows[1::2].reshape(-1, 2)):
         p = Plan(cfg.n, cfg.M, cfg.w, sel, None, probe, precision="c64")
-        p.set_stream(torch.cuda.current_stream().cuda_stream)   # ordered after torch's writes of z / v
         p.simulate(obj, copy_out=False)
         plans.append(p)
     g = torch.Generator(device="cpu").manual_seed(3)
@@ -139,6 +138,7 @@ def test_config5_full_properties():
     z += 0.05 * torch.complex(torch.rand(cfg.n, cfg.n, generator=g) - 0.5,
                               torch.rand(cfg.n, cfg.n, generator=g) - 0.5).cuda()
     grads = [torch.empty_like(z) for _ in plans]
+    torch.cuda.synchronize()   # the plans run on their own streams: z / v must be written first
     vals = [p.evaluate_device(z, gr) for p, gr in zip(plans, grads)]
     # (1) determinism
     g2 = torch.empty_like(z)
@@ -151,6 +151,7 @@ def test_config5_full_properties():
     # (3) shift
     v = 0.01 * torch.complex(torch.rand(cfg.n, cfg.n, generator=g), torch.rand(cfg.n, cfg.n, generator=g)).cuda()
     gv = torch.empty_like(z)
+    torch.cuda.synchronize()
     val_v = plans[0].evaluate_device(z, gv, v=v)
     dot = float(torch.sum(v.real.double() * z.real.double() + v.imag.double() * z.imag.double()))
     assert rel(val_v, vals[0] - dot) <= 1e-9
@@ -203,3 +204,33 @@ def test_rmw_matches_stash_path(oracle, monkeypatch):
     assert rel(va, vb) <= 1e-6 and rel_l2(ga, gb) <= 1e-5
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("bands", ["1", "3", "8"])
+def test_rmw_banded_host_eval_bitwise(oracle, monkeypatch, bands):
+    """ptg_eval with host buffers on an RMW plan (banded upload / per-band
+    launches / early download) = the device evaluation, bitwise."""
+    import torch
+
+    from paper_1810_05628_b200 import Plan, synth
+    M, steps, step = 256, 5, 48
+    n = (steps - 1) * step + M + 40
+    cfg = synth.Config(0, n, M, steps, step, 6.0, M / 4, 0.001, "c64", jitter=3)
+    obj, probe, pos = synth.make_inputs(cfg)
+    probe, obj = _r64(probe), _r64(obj)
+    data = oracle.simulate(n, M, M, pos, obj, probe).astype(np.float32)
+    z = _r64(obj * 0.9 + 0.05 * rand_field(n, 7))
+    monkeypatch.setenv("PTG_NO_PLANES", "1")
+    monkeypatch.setenv("PTG_RMW_BANDS", bands)
+    plan = Plan(n, M, M, pos, data, probe, precision="c64")
+    hv, hg = plan.evaluate(z)
+    zt = torch.from_numpy(z.astype(np.complex64)).cuda()
+    gt = torch.empty_like(zt)
+    torch.cuda.synchronize()
+    dv = plan.evaluate_device(zt, gt)
+    assert hv == dv
+    assert np.array_equal(hg, gt.cpu().numpy().astype(np.complex128))
+    prob = oracle.Problem(n, M, M, pos, data.astype(np.float64), probe)
+    wv, wg = oracle.evaluate(prob, z)
+    assert rel(hv, wv) <= C64_VAL and rel_l2(hg, wg) <= C64_GRAD
+    plan.close()
