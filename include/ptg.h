@@ -135,6 +135,11 @@ int ptg_project_modulus(ptg_plan *plan, const double *z, int k, double *frame);
 int ptg_simulate(ptg_plan *plan, const double *z, double *data_out);
 int ptg_simulate_device(ptg_plan *plan, const void *z);
 
+/* fft2 / ifft2 (field.hpp:91-93; kernels.cpp:34-85 convention: unnormalised
+ * forward, inverse x 1/n^2) of a host complex128 n x n field on the current
+ * device, with the objective kernels' own 2-D FFT (n a power of two <= 64) */
+int ptg_fft2(const double *in, int n, int inverse, double *out);
+
 /* ---------------------------------------------------------------- noise */
 /* addNoise (forward.hpp:44-48, forward.cpp:56-86) in place on the plan's
  * resident intensities (the amplitudes are rebuilt): per pattern
@@ -160,6 +165,11 @@ int ptg_uniform01_stream(uint64_t seed, size_t count, double *out);
  * (host out; for pinning the generator against numpy.random.Philox) */
 int ptg_philox4x64(int device, const uint64_t ctr[4], const uint64_t key[2], size_t nblocks, uint64_t *out);
 
+/* IterationCallback (solvers.hpp:70-71): (user, iteration index, host
+ * complex128 iterate n*n, objective value, weighted evaluations so far); fired
+ * for the initial point (index 0) and after every iteration / sweep / cycle. */
+typedef void (*ptg_iter_cb)(void *user, int iter, const double *z, double value, double weighted);
+
 /* ----------------------------------------------------------------- PIE */
 typedef struct { double weighted, value, gnorm; } ptg_hist;
 
@@ -169,6 +179,10 @@ typedef struct { double weighted, value, gnorm; } ptg_hist;
 int ptg_pie(ptg_plan *plan, double *z, double gamma, int sweeps, double max_weighted,
             double *final_value, ptg_hist *hist, int hist_cap, int *hist_len,
             double *weighted, int *reason);
+/* the same with an IterationCallback (cb may be NULL) */
+int ptg_pie_cb(ptg_plan *plan, double *z, double gamma, int sweeps, double max_weighted,
+               double *final_value, ptg_hist *hist, int hist_cap, int *hist_len, double *weighted,
+               int *reason, ptg_iter_cb cb, void *user);
 /* one raw sweep on a device object (no diagnostics, no accounting) */
 int ptg_pie_sweep_device(ptg_plan *plan, void *z, double gamma);
 
@@ -259,11 +273,24 @@ int ptg_lbfgs(ptg_plan *plan, int metric, const double *v, const double *z0,
               const ptg_solver_cfg *cfg, double *z_out, double *grad_out, ptg_report *rep,
               ptg_hist *hist, int hist_cap);
 
+/* lbfgs with the reference's full signature (solvers.hpp:92-95): warmStart
+ * (warm_value + host complex128 warm_grad, both or neither: the evaluation at
+ * z0, not charged again) and an IterationCallback (cb may be NULL).
+ * grad_out receives finalEval.gradient. */
+int ptg_lbfgs_ex(ptg_plan *plan, int metric, const double *v, const double *z0, const double *warm_value,
+                 const double *warm_grad, const ptg_solver_cfg *cfg, double *z_out, double *grad_out,
+                 ptg_report *rep, ptg_hist *hist, int hist_cap, ptg_iter_cb cb, void *user);
 /* truncatedNewton (solvers.hpp:101-104): Newton-CG with finite-difference
  * Hessian-vector products (one counted gradient evaluation each), GPU-resident. */
 int ptg_truncated_newton(ptg_plan *plan, int metric, const double *v, const double *z0,
                          const ptg_solver_cfg *cfg, double *z_out, double *grad_out, ptg_report *rep,
                          ptg_hist *hist, int hist_cap);
+
+/* truncatedNewton with warmStart and IterationCallback (solvers.hpp:101-104) */
+int ptg_truncated_newton_ex(ptg_plan *plan, int metric, const double *v, const double *z0,
+                            const double *warm_value, const double *warm_grad, const ptg_solver_cfg *cfg,
+                            double *z_out, double *grad_out, ptg_report *rep, ptg_hist *hist, int hist_cap,
+                            ptg_iter_cb cb, void *user);
 
 typedef struct ptg_hier ptg_hier;
 /* buildHierarchy (multigrid.hpp:61-62): coarse levels built ON DEVICE by
@@ -275,6 +302,17 @@ int ptg_hier_level(ptg_hier *h, int level, ptg_plan **plan_out);
 /* mgoptDriver (multigrid.hpp:93-95), GPU-resident */
 int ptg_mgopt_driver(ptg_hier *h, const double *z0, const ptg_driver_cfg *cfg, double *z_out,
                      ptg_report *rep, ptg_hist *hist, int hist_cap);
+/* mgoptDriver with an IterationCallback (one call per completed cycle) and
+ * finalEval.gradient (grad_out, one uncounted evaluation; may be NULL) */
+int ptg_mgopt_driver_ex(ptg_hier *h, const double *z0, const ptg_driver_cfg *cfg, double *z_out,
+                        double *grad_out, ptg_report *rep, ptg_hist *hist, int hist_cap, ptg_iter_cb cb,
+                        void *user);
+/* mgoptCycle (multigrid.hpp:78-80) at any level with shift v (NULL = zero):
+ * host complex128 buffers of that level's side; warmStart optional (both the
+ * value and the gradient, or neither).  Returns the cycle's final iterate,
+ * shifted value and gradient (CycleResult). ConfigError for a bad level. */
+int ptg_mgopt_cycle(ptg_hier *h, int level, const double *z, const double *v, const double *warm_value,
+                    const double *warm_grad, double *z_out, double *value_out, double *grad_out, ptg_report *rep);
 /* one top-level V-cycle (mgoptCycle, multigrid.hpp:78-80) on device buffers:
  * z in/out (level-0 precision), warm (value, grad) in/out. */
 int ptg_mgopt_cycle_device(ptg_hier *h, void *z, double *value, void *grad, ptg_report *rep);

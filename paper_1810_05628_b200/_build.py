@@ -87,23 +87,50 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
 
 
 CPP = os.path.join(PKG, "cpp")
-CPP_TEST = os.path.join(LIBDIR, "test_ptycho_b200")
+CPP_INC = os.path.join(CPP, "include")
+SHIM = os.path.join(CPP, "doctest_shim")
+EXT_TEST = os.path.join(LIBDIR, "test_dropin_ext")
+REF_TEST = os.path.join(LIBDIR, "ref_tests_dropin")
+REF_TESTS_DIR = "/root/reference/proj/tests"
+REF_TEST_FILES = ("test_objectives.cpp", "test_solvers.cpp", "test_multigrid.cpp")
+
+
+def _cxx():
+    return shutil.which("g++", path="/usr/bin") or "g++"
+
+
+def _cpp_headers():
+    out = [os.path.join(ROOT, "include", "ptg.h"), os.path.join(SHIM, "doctest.h"), LIB]
+    for d, _, fs in os.walk(CPP_INC):
+        out += [os.path.join(d, f) for f in fs if f.endswith(".hpp")]
+    return out
 
 
 def build_cpp_tests() -> str:
-    """Reference-style C++ tests of the drop-in header, linked against libptg.so."""
-    src = os.path.join(CPP, "test_shim.cpp")
-    deps = [src, os.path.join(CPP, "ptycho_b200.hpp"), os.path.join(ROOT, "include", "ptg.h"), LIB]
-    if not _stale(CPP_TEST, deps):
-        return CPP_TEST
-    gxx = shutil.which("g++", path="/usr/bin") or "g++"
-    cmd = [gxx, "-std=c++20", "-O2", "-Wall", "-I" + os.path.join(ROOT, "include"), "-I" + CPP, src,
-           "-o", CPP_TEST, "-L" + LIBDIR, "-lptg", "-Wl,-rpath,$ORIGIN"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("C++ drop-in test build failed")
-    return CPP_TEST
+    """C++ tests of the drop-in headers (cpp/include/ptycho), linked to libptg.so:
+    test_dropin_ext (the additive API) and, where the reference sources exist,
+    ref_tests_dropin = the reference's UNMODIFIED unit tests
+    (proj/tests/test_objectives.cpp, test_solvers.cpp, test_multigrid.cpp,
+    compiled in place with the doctest shim; never copied) -- the binary
+    travels to the GPU box with the rest of lib/."""
+    flags = ["-std=c++20", "-O2", "-Wall", "-I" + CPP_INC, "-I" + CPP, "-I" + SHIM, "-I" + os.path.join(ROOT, "include")]
+    link = ["-L" + LIBDIR, "-lptg", "-Wl,-rpath,$ORIGIN"]
+    deps = _cpp_headers()
+    src = os.path.join(CPP, "test_dropin_ext.cpp")
+    if _stale(EXT_TEST, deps + [src]):
+        r = subprocess.run([_cxx(), *flags, src, "-o", EXT_TEST, *link], capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("C++ drop-in extension test build failed")
+    if os.path.isdir(REF_TESTS_DIR):
+        srcs = [os.path.join(REF_TESTS_DIR, f) for f in REF_TEST_FILES] + [os.path.join(CPP, "ref_tests_main.cpp")]
+        if _stale(REF_TEST, deps + srcs):
+            cmd = [_cxx(), *flags, "-I" + REF_TESTS_DIR, *srcs, "-o", REF_TEST, *link]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError("reference unit tests against the drop-in failed to build")
+    return EXT_TEST
 
 
 if __name__ == "__main__":

@@ -105,7 +105,8 @@ EXPORTS = [
     "ptg_plan_set_timing", "ptg_plan_get_timing",
     "ptg_eval", "ptg_eval_device", "ptg_project_modulus", "ptg_simulate", "ptg_simulate_device",
     "ptg_add_noise", "ptg_add_poisson", "ptg_philox4x64", "ptg_uniform01_stream",
-    "ptg_pie", "ptg_pie_sweep_device",
+    "ptg_pie", "ptg_pie_cb", "ptg_pie_sweep_device", "ptg_fft2",
+    "ptg_lbfgs_ex", "ptg_truncated_newton_ex", "ptg_mgopt_driver_ex", "ptg_mgopt_cycle",
     "ptg_restrict_field", "ptg_prolong_field", "ptg_restrict_data",
     "ptg_restrict_field_device", "ptg_prolong_field_device", "ptg_restrict_data_device",
     "ptg_halo_bytes", "ptg_halo_pack", "ptg_halo_unpack",

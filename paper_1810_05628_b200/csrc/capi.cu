@@ -60,6 +60,24 @@ void fill_report(ptg_report* rep, const ptg::Counter& c, double value, int reaso
     rep->hist_len = hist_len;
 }
 
+// IterationCallback bridge: while alive, the top-level solver's history
+// points download the device iterate (complex128) and call the user's function
+struct CbScope {
+    ptg::IterHook fn;
+    const ptg::IterHook* prev;
+    CbScope(ptg::Plan& p, ptg_iter_cb cb, void* user) : prev(ptg::g_iter_hook) {
+        if (!cb) return;
+        fn = [&p, cb, user](int it, const void* zd, double val, double w) {
+            std::vector<double> h(2 * p.nn());
+            ptg::plan_download_c128(p, zd, h.data());
+            PTG_CUDA(cudaStreamSynchronize(p.stream));
+            cb(user, it, h.data(), val, w);
+        };
+        ptg::g_iter_hook = &fn;
+    }
+    ~CbScope() { ptg::g_iter_hook = prev; }
+};
+
 int copy_hist(const std::vector<ptg_hist>& h, ptg_hist* out, int cap) {
     const int n = (int)h.size();
     if (out)
@@ -329,6 +347,13 @@ int ptg_philox4x64(int device, const uint64_t ctr[4], const uint64_t key[2], siz
 int ptg_pie(ptg_plan* plan, double* z, double gamma, int sweeps, double max_weighted,
             double* final_value, ptg_hist* hist, int hist_cap, int* hist_len, double* weighted,
             int* reason) {
+    return ptg_pie_cb(plan, z, gamma, sweeps, max_weighted, final_value, hist, hist_cap, hist_len, weighted, reason,
+                      nullptr, nullptr);
+}
+
+int ptg_pie_cb(ptg_plan* plan, double* z, double gamma, int sweeps, double max_weighted,
+               double* final_value, ptg_hist* hist, int hist_cap, int* hist_len, double* weighted,
+               int* reason, ptg_iter_cb cb, void* user) {
     return guard([&] {
         ptg::Plan& p = P(plan);
         if (gamma < 0.0) ptg::raise(PTG_ERR_CONFIG, "pie: gamma must be non-negative");
@@ -342,15 +367,16 @@ int ptg_pie(ptg_plan* plan, double* z, double gamma, int sweeps, double max_weig
             const double val = ptg::plan_read_scalar(p, p.value.as<double>());
             return val;
         };
+        CbScope cbs(p, cb, user);
         double val = diag();
-        h.push_back({ctr.weighted, val, std::sqrt(ptg::plan_dot(p, gd.p, gd.p, len))});
+        ptg::hist_push(&h, ctr, val, std::sqrt(ptg::plan_dot(p, gd.p, gd.p, len)), zd.p);
         int rsn = PTG_STOP_MAXITERS;
         for (int sweep = 1; sweep <= sweeps; ++sweep) {
             ptg::plan_pie_sweep(p, zd.p, gamma);
             if (ptg::plan_nonfinite(p, zd.p, len)) ptg::raise(PTG_ERR_NUMERIC, "non-finite iterate in pie");
             ctr.record(0, 1.0);   // one sweep = one fine-level evaluation
             val = diag();
-            h.push_back({ctr.weighted, val, std::sqrt(ptg::plan_dot(p, gd.p, gd.p, len))});
+            ptg::hist_push(&h, ctr, val, std::sqrt(ptg::plan_dot(p, gd.p, gd.p, len)), zd.p);
             if (ctr.weighted >= max_weighted) {
                 rsn = PTG_STOP_BUDGET;
                 break;
@@ -462,6 +488,77 @@ int ptg_lbfgs(ptg_plan* plan, int metric, const double* v, const double* z0,
         if (grad_out) ptg::plan_download_c128(p, go.p, grad_out);
         PTG_CUDA(cudaStreamSynchronize(p.stream));
         fill_report(rep, ctr, o.value, o.reason, copy_hist(h, hist, hist_cap));
+    });
+}
+
+namespace {
+int solve_ex(bool tn, ptg_plan* plan, int metric, const double* v, const double* z0, const double* warm_value,
+             const double* warm_grad, const ptg_solver_cfg* cfg, double* z_out, double* grad_out, ptg_report* rep,
+             ptg_hist* hist, int hist_cap, ptg_iter_cb cb, void* user) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        ptg_solver_cfg c;
+        if (cfg) c = *cfg;
+        else ptg_solver_cfg_default(&c);
+        if ((warm_value == nullptr) != (warm_grad == nullptr))
+            ptg::raise(PTG_ERR_CONFIG, "warm start needs both the value and the gradient");
+        const size_t len = p.nn();
+        ptg::DVec zd(p, len), vd, wg, zo(p, len), go(p, len);
+        ptg::plan_upload_c128(p, z0, zd.p);
+        if (v) {
+            vd.alloc(p, len);
+            ptg::plan_upload_c128(p, v, vd.p);
+        }
+        if (warm_grad) {
+            wg.alloc(p, len);
+            ptg::plan_upload_c128(p, warm_grad, wg.p);
+        }
+        ptg::DObj obj;
+        obj.plan = &p;
+        obj.metric = metric;
+        obj.v = v ? vd.p : nullptr;
+        ptg::Counter ctr;
+        std::vector<ptg_hist> h;
+        CbScope cbs(p, cb, user);
+        ptg::SolveOut o = tn ? ptg::d_truncated_newton(obj, zd.p, c, ctr, warm_value, wg.p, zo.p, go.p, &h)
+                             : ptg::d_lbfgs(obj, zd.p, c, ctr, warm_value, wg.p, zo.p, go.p, &h);
+        if (z_out) ptg::plan_download_c128(p, zo.p, z_out);
+        if (grad_out) ptg::plan_download_c128(p, go.p, grad_out);
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+        fill_report(rep, ctr, o.value, o.reason, copy_hist(h, hist, hist_cap));
+    });
+}
+}  // namespace
+
+int ptg_lbfgs_ex(ptg_plan* plan, int metric, const double* v, const double* z0, const double* warm_value,
+                 const double* warm_grad, const ptg_solver_cfg* cfg, double* z_out, double* grad_out,
+                 ptg_report* rep, ptg_hist* hist, int hist_cap, ptg_iter_cb cb, void* user) {
+    return solve_ex(false, plan, metric, v, z0, warm_value, warm_grad, cfg, z_out, grad_out, rep, hist, hist_cap, cb,
+                    user);
+}
+
+int ptg_truncated_newton_ex(ptg_plan* plan, int metric, const double* v, const double* z0,
+                            const double* warm_value, const double* warm_grad, const ptg_solver_cfg* cfg,
+                            double* z_out, double* grad_out, ptg_report* rep, ptg_hist* hist, int hist_cap,
+                            ptg_iter_cb cb, void* user) {
+    return solve_ex(true, plan, metric, v, z0, warm_value, warm_grad, cfg, z_out, grad_out, rep, hist, hist_cap, cb,
+                    user);
+}
+
+int ptg_fft2(const double* in, int n, int inverse, double* out) {
+    return guard([&] {
+        if (!in || !out) ptg::raise(PTG_ERR_CONFIG, "fft2: null pointer");
+        int dev = 0;
+        PTG_CUDA(cudaGetDevice(&dev));
+        ptg::check_device_public(dev);
+        if (n < 1) ptg::raise(PTG_ERR_GEOMETRY, "fft2: grid side must be a positive power of two, got " + std::to_string(n));
+        const size_t bytes = (size_t)n * n * 16;
+        ptg::DevMem a, b;
+        a.alloc(bytes);
+        b.alloc(bytes);
+        PTG_CUDA(cudaMemcpy(a.p, in, bytes, cudaMemcpyHostToDevice));
+        ptg::dev_fft2(a.p, n, inverse != 0, b.p, nullptr);
+        PTG_CUDA(cudaMemcpy(out, b.p, bytes, cudaMemcpyDeviceToHost));
     });
 }
 
@@ -591,6 +688,66 @@ int ptg_mgopt_driver(ptg_hier* hh, const double* z0, const ptg_driver_cfg* cfg, 
         std::vector<ptg_hist> hv;
         ptg::SolveOut o = ptg::d_mgopt_driver(h, zd.p, c, ctr, zo.p, &hv);
         if (z_out) ptg::plan_download_c128(p, zo.p, z_out);
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+        fill_report(rep, ctr, o.value, o.reason, copy_hist(hv, hist, hist_cap));
+    });
+}
+
+int ptg_mgopt_cycle(ptg_hier* hh, int level, const double* z, const double* v, const double* warm_value,
+                    const double* warm_grad, double* z_out, double* value_out, double* grad_out, ptg_report* rep) {
+    return guard([&] {
+        if (!hh) ptg::raise(PTG_ERR_CONFIG, "null hierarchy");
+        ptg::Hier& h = *hh->h;
+        if (level < 0 || level >= h.depth()) ptg::raise(PTG_ERR_CONFIG, "mgoptCycle: bad level");
+        if ((warm_value == nullptr) != (warm_grad == nullptr))
+            ptg::raise(PTG_ERR_CONFIG, "warm start needs both the value and the gradient");
+        P(hh->fine);
+        sync_streams(h);
+        ptg::Plan& p = *h.levels[level];
+        const size_t len = p.nn();
+        ptg::DVec zd(p, len), vd, wg, zo(p, len), go(p, len);
+        ptg::plan_upload_c128(p, z, zd.p);
+        if (v) {
+            vd.alloc(p, len);
+            ptg::plan_upload_c128(p, v, vd.p);
+        }
+        if (warm_grad) {
+            wg.alloc(p, len);
+            ptg::plan_upload_c128(p, warm_grad, wg.p);
+        }
+        ptg::Counter ctr;
+        const double val = ptg::d_mgopt_cycle(h, level, zd.p, v ? vd.p : nullptr, ctr, warm_value, wg.p, zo.p, go.p);
+        if (z_out) ptg::plan_download_c128(p, zo.p, z_out);
+        if (grad_out) ptg::plan_download_c128(p, go.p, grad_out);
+        PTG_CUDA(cudaStreamSynchronize(p.stream));
+        if (value_out) *value_out = val;
+        fill_report(rep, ctr, val, PTG_STOP_MAXITERS, 0);
+    });
+}
+
+int ptg_mgopt_driver_ex(ptg_hier* hh, const double* z0, const ptg_driver_cfg* cfg, double* z_out, double* grad_out,
+                        ptg_report* rep, ptg_hist* hist, int hist_cap, ptg_iter_cb cb, void* user) {
+    return guard([&] {
+        if (!hh) ptg::raise(PTG_ERR_CONFIG, "null hierarchy");
+        ptg::Hier& h = *hh->h;
+        ptg::Plan& p = P(hh->fine);
+        sync_streams(h);
+        ptg_driver_cfg c;
+        if (cfg) c = *cfg;
+        else ptg_driver_cfg_default(&c);
+        const size_t len = p.nn();
+        ptg::DVec zd(p, len), zo(p, len);
+        ptg::plan_upload_c128(p, z0, zd.p);
+        ptg::Counter ctr;
+        std::vector<ptg_hist> hv;
+        CbScope cbs(p, cb, user);
+        ptg::SolveOut o = ptg::d_mgopt_driver(h, zd.p, c, ctr, zo.p, &hv);
+        if (z_out) ptg::plan_download_c128(p, zo.p, z_out);
+        if (grad_out) {   // finalEval's gradient: one uncounted evaluation at the final iterate
+            ptg::DVec go(p, len);
+            ptg::plan_eval(p, h.metric, zo.p, nullptr, go.p, p.value.as<double>());
+            ptg::plan_download_c128(p, go.p, grad_out);
+        }
         PTG_CUDA(cudaStreamSynchronize(p.stream));
         fill_report(rep, ctr, o.value, o.reason, copy_hist(hv, hist, hist_cap));
     });

@@ -20,7 +20,13 @@
 
 namespace ptg {
 
-enum SpectralOp { OP_DISTANCE = 0, OP_INTENSITY = 1, OP_SIMULATE = 2, OP_PROJECT = 3 };
+enum SpectralOp {
+    OP_DISTANCE = 0, OP_INTENSITY = 1, OP_SIMULATE = 2, OP_PROJECT = 3,
+    // plain 2-D transforms of the gathered frame (fft2 / ifft2, field.hpp:91-93):
+    // the same smem FFT and 1/M^2 scaling as the projection's inverse, so
+    // ifft2 of a projection's spectrum is bitwise the projection
+    OP_FFT_FWD = 4, OP_FFT_INV = 5
+};
 
 template <typename T>
 struct FrameArgs {
@@ -129,6 +135,16 @@ __global__ void __launch_bounds__(NT) frame_kernel(FrameArgs<T> a) {
         buf[r * S + c] = v;
     }
     __syncthreads();
+    if constexpr (OP == OP_FFT_FWD || OP == OP_FFT_INV) {
+        fft2d_smem<T, M, NT, OP == OP_FFT_INV>(buf, S, tw);
+        C* out = a.frame_out + (size_t)j * M * M;
+        const T sc = T(1) / (T(M) * T(M));
+        for (int idx = threadIdx.x; idx < M * M; idx += NT) {
+            const C v = buf[(idx / M) * S + idx % M];
+            out[idx] = OP == OP_FFT_INV ? cscale(v, sc) : v;
+        }
+        return;
+    }
     fft2d_smem<T, M, NT, false>(buf, S, tw);
 
     if constexpr (OP == OP_SIMULATE) {

@@ -1884,6 +1884,30 @@ void plan_project(Plan& p, const void* z, int k, void* out) {
     else project_t<double>(p, z, k, out);
 }
 
+// ------------------------------------------------------------------ fft2
+// fft2 / ifft2 (field.hpp:91-93, kernels.cpp:34-85) of one n x n complex128
+// field on the device: the objective kernels' own 2-D FFT (single-CTA frame
+// kernel, n <= 64 in complex128)
+void dev_fft2(const void* in, int n, bool inverse, void* out, cudaStream_t s) {
+    if (!is_pow2(n)) raise(PTG_ERR_GEOMETRY, "fft2: grid side must be a positive power of two, got " + std::to_string(n));
+    if (!frame_single_cta(PTG_C128, n))
+        raise(PTG_ERR_CONFIG, "fft2: n=" + std::to_string(n) + " exceeds the single-CTA complex128 transform (n <= 64)");
+    DevMem pos;
+    pos.alloc(sizeof(int2));
+    PTG_CUDA(cudaMemsetAsync(pos.p, 0, sizeof(int2), s));
+    FrameArgs<double> a{};
+    a.z = static_cast<const double2*>(in);
+    a.pos = pos.as<const int2>();
+    a.frame_out = static_cast<double2*>(out);
+    a.n = n;
+    a.w = n;
+    a.first = 0;
+    if (inverse) launch_frame_m<double, OP_FFT_INV>(n, a, 1, s);
+    else launch_frame_m<double, OP_FFT_FWD>(n, a, 1, s);
+    count_launch();
+    PTG_CUDA(cudaStreamSynchronize(s));   // `pos` is freed on return
+}
+
 // -------------------------------------------------------------------- PIE
 // z_win += weight o (Pi(psi) - psi) for one position (multi-pass frames)
 template <typename T>

@@ -210,6 +210,8 @@ void plan_eval(Plan& p, int metric, const void* z, const void* v, void* grad, do
 void plan_eval_host(Plan& p, int metric, const double* z, const double* v, double* value, double* grad);
 void plan_simulate(Plan& p, const void* z);
 void plan_project(Plan& p, const void* z, int k, void* frame_out);
+// fft2 / ifft2 of a device n x n complex128 field (synchronises s)
+void dev_fft2(const void* in, int n, bool inverse, void* out, cudaStream_t s);
 // one PIE sweep in place on device object z
 void plan_pie_sweep(Plan& p, void* z, double gamma);
 

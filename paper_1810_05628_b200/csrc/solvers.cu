@@ -11,6 +11,8 @@
 
 namespace ptg {
 
+thread_local const IterHook* g_iter_hook = nullptr;
+
 // PTG_LBFGS_DEBUG=1: host time inside the line-search synchronisations vs the
 // whole LBFGS call (dev instrumentation)
 static thread_local double g_sync_us = 0.0, g_graph_us = 0.0;   // one context per host thread
@@ -185,7 +187,7 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
     const double grad_floor = cfg.grad_tol_abs * (1.0 + std::sqrt(z0sq));
     const double g0 = std::sqrt(gsq);
     double gnorm = g0;
-    if (hist) hist->push_back({ctr.weighted, cur, gnorm});
+    hist_push(hist, ctr, cur, gnorm, z0);
     auto satisfied = [&](double gn) { return gn <= std::max(cfg.grad_tol_rel * g0, grad_floor); };
     SolveOut out;
     out.reason = PTG_STOP_MAXITERS;
@@ -485,7 +487,7 @@ SolveOut d_lbfgs(const DObj& obj, const void* z0, const ptg_solver_cfg& cfg, Cou
             ++iters_done;
             cur = lsr.value;
             gnorm = std::sqrt(stats_h[3]);
-            if (hist) hist->push_back({ctr.weighted, cur, gnorm});
+            hist_push(hist, ctr, cur, gnorm, z.p);
             if (satisfied(gnorm)) {
                 out.reason = PTG_STOP_TOLERANCE;
                 break;
@@ -536,7 +538,7 @@ SolveOut d_truncated_newton(const DObj& obj, const void* z0, const ptg_solver_cf
     const double grad_floor = cfg.grad_tol_abs * (1.0 + dnorm(p, z0));
     const double g0 = dnorm(p, g.p);
     double gnorm = g0;
-    if (hist) hist->push_back({ctr.weighted, cur, gnorm});
+    hist_push(hist, ctr, cur, gnorm, z0);
     auto satisfied = [&](double gn) { return gn <= std::max(cfg.grad_tol_rel * g0, grad_floor); };
     SolveOut out;
     out.reason = PTG_STOP_MAXITERS;
@@ -586,7 +588,7 @@ SolveOut d_truncated_newton(const DObj& obj, const void* z0, const ptg_solver_cf
             std::swap(g, ng);
             cur = lsr.value;
             gnorm = dnorm(p, g.p);
-            if (hist) hist->push_back({ctr.weighted, cur, gnorm});
+            hist_push(hist, ctr, cur, gnorm, z.p);
             if (satisfied(gnorm)) {
                 out.reason = PTG_STOP_TOLERANCE;
                 break;
@@ -731,7 +733,7 @@ SolveOut d_mgopt_driver(Hier& h, const void* z0, const ptg_driver_cfg& cfg, Coun
     const double g0 = dnorm(p, g.p);
     const double grad_floor = cfg.grad_tol_abs * (1.0 + dnorm(p, z0));
     double gnorm = g0;
-    if (hist) hist->push_back({ctr.weighted, cur, gnorm});
+    hist_push(hist, ctr, cur, gnorm, z.p);
     SolveOut out;
     out.reason = PTG_STOP_MAXITERS;
     if (gnorm <= std::max(cfg.grad_tol_rel * g0, grad_floor)) {
@@ -742,7 +744,7 @@ SolveOut d_mgopt_driver(Hier& h, const void* z0, const ptg_driver_cfg& cfg, Coun
             std::swap(z, nz);
             std::swap(g, ng);
             gnorm = dnorm(p, g.p);
-            if (hist) hist->push_back({ctr.weighted, cur, gnorm});
+            hist_push(hist, ctr, cur, gnorm, z.p);
             if (gnorm <= std::max(cfg.grad_tol_rel * g0, grad_floor)) {
                 out.reason = PTG_STOP_TOLERANCE;
                 break;

@@ -160,6 +160,19 @@ struct Hier {
     int depth() const { return (int)levels.size(); }
 };
 
+// IterationCallback (solvers.hpp:70-71) of the top-level solver call: set by
+// the C-ABI for the duration of one call; fired wherever a top-level solver
+// appends a history point (initial point + one per iteration / cycle) with
+// the device iterate.  Nested solvers (smoothers, coarse solves) keep no
+// history and so never fire it.
+using IterHook = std::function<void(int iter, const void* z_dev, double value, double weighted)>;
+extern thread_local const IterHook* g_iter_hook;
+inline void hist_push(std::vector<ptg_hist>* hist, const Counter& ctr, double value, double gnorm, const void* z_dev) {
+    if (!hist) return;
+    hist->push_back({ctr.weighted, value, gnorm});
+    if (g_iter_hook) (*g_iter_hook)((int)hist->size() - 1, z_dev, value, ctr.weighted);
+}
+
 std::unique_ptr<Hier> hier_build(Plan& fine, int metric, int depth, const ptg_mg_cfg& opt);
 // multigrid.cpp:117-169 ; v may be null (= zero shift)
 double d_mgopt_cycle(Hier& h, int level, const void* z, const void* v, Counter& ctr,
