@@ -197,6 +197,45 @@ int ptg_restrict_field_device(int precision, const void *fine, int n, void *coar
 int ptg_prolong_field_device(int precision, const void *coarse, int nH, void *fine, void *stream);
 int ptg_restrict_data_device(int dtype, const void *fine, int N, int M, void *coarse, void *stream);
 
+/* ------------------------------------------------------------ multi-GPU */
+/* SURVEY 8(e) / north_star: one process per GPU, scan positions sharded,
+ * NCCL inside libptg (bound at run time: libnccl.so.2).  No reference
+ * counterpart (the reference is single-process).
+ *
+ * Partition (ptg_shard_layout, host-only): the global scan (positions in scan
+ * order, window rows non-decreasing between rows of the scan) is cut at
+ * scan-row boundaries into `world` contiguous blocks of about N / world
+ * positions; rank r evaluates block r.
+ *   PTG_SHARD_REPLICATED  every rank holds the whole n x n object; after its
+ *                         frames one NCCL allreduce of [gradient | value] --
+ *                         north_star's layout.  The solvers run replicated on
+ *                         the allreduced values (identical on every rank).
+ *   PTG_SHARD_BANDS       rank r holds object rows [row0, row0 + rows): its
+ *                         own rows (up to the next rank's first window row)
+ *                         plus the halo its windows reach below them; halo
+ *                         gradient rows go to rank r + 1 (NCCL send/recv),
+ *                         the value is one scalar allreduce.  Device buffers
+ *                         (z, v, grad) are rows x n.  Needs own rows >= the
+ *                         halo on every rank.  complex64, M = 128 / 256, w = M
+ *                         (the persistent RMW path); evaluation only. */
+enum ptg_shard { PTG_SHARD_NONE = 0, PTG_SHARD_REPLICATED = 1, PTG_SHARD_BANDS = 2 };
+typedef struct ptg_comm ptg_comm;
+/* ncclGetUniqueId on one rank; distribute the 128 bytes, then ptg_comm_init everywhere */
+int ptg_comm_unique_id(unsigned char id[128]);
+int ptg_comm_init(const unsigned char id[128], int world, int rank, int device, ptg_comm **out);
+int ptg_comm_destroy(ptg_comm *comm);
+/* out[6] = {pos_begin, pos_end, row0, rows, own_rows, halo_prev} of `rank` */
+int ptg_shard_layout(int n, int w, int N, const int32_t *positions, int world, int rank, int layout, int out[6]);
+/* this rank's plan of the GLOBAL problem `desc` (all N positions; desc->data
+ * NULL or the rank's own patterns [pos_begin, pos_end) in scan order) */
+int ptg_plan_create_sharded(const ptg_plan_desc *desc, int world, int rank, int layout, ptg_plan **out);
+/* bind the communicator: every later evaluation (ptg_eval / _device) of this
+ * plan returns the GLOBAL value and this rank's gradient (REPLICATED: the
+ * whole gradient; BANDS: its rows, own rows final) */
+int ptg_plan_bind_comm(ptg_plan *plan, ptg_comm *comm);
+/* BANDS: fill the iterate's halo rows [own_rows, rows) from rank + 1 (device z) */
+int ptg_band_sync_halo(ptg_plan *plan, void *z_dev);
+
 /* ----------------------------------------------- multi-GPU band exchange */
 /* No reference counterpart (the reference is single-process): helpers of the
  * band decomposition of SURVEY 8(e) (paper_1810_05628_b200/sharding.py).  A

@@ -10,9 +10,10 @@ from .ptycho import (DISTANCE, INTENSITY, ConfigError, CudaError, DomainError, E
                      GeometryError, Hierarchy, IoError, MetricError, NumericError, Plan,
                      SolverReport, device_count, prolong_field, restrict_data, restrict_field,
                      write_ptyf, metrics, metrics_device, relative_error, magnitude_rel_error,
-                     phase_ssim, canonical_phase)
+                     phase_ssim, canonical_phase, Comm, shard_layout)
 
 __all__ = ["Plan", "Hierarchy", "SolverReport", "restrict_field", "prolong_field", "restrict_data",
            "DISTANCE", "INTENSITY", "Error", "ConfigError", "GeometryError", "DomainError",
            "MetricError", "IoError", "NumericError", "CudaError", "device_count", "write_ptyf",
-           "metrics", "metrics_device", "relative_error", "magnitude_rel_error", "phase_ssim", "canonical_phase"]
+           "metrics", "metrics_device", "relative_error", "magnitude_rel_error", "phase_ssim", "canonical_phase",
+           "Comm", "shard_layout"]

@@ -77,7 +77,7 @@ def build(verbose: bool = False, jobs: int = 8) -> str:
             with open(os.path.join(OBJDIR, os.path.basename(cmd[-1]) + ".ptxas.txt"), "w") as f:
                 f.write(log)
     if cmds or not os.path.exists(LIB):
-        link = [nvcc(), *host_cxx(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+        link = [nvcc(), *host_cxx(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-ldl"]
         r = subprocess.run(link, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

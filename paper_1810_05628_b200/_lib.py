@@ -16,6 +16,7 @@ PTG_OK = 0
 PTG_C64, PTG_C128 = 0, 1
 PTG_F32, PTG_F64 = 0, 1
 PTG_DISTANCE, PTG_INTENSITY = 0, 1
+PTG_SHARD_NONE, PTG_SHARD_REPLICATED, PTG_SHARD_BANDS = 0, 1, 2
 
 
 # --- exception hierarchy mirroring /root/reference/proj/include/ptycho/errors.hpp:12-43
@@ -110,6 +111,8 @@ EXPORTS = [
     "ptg_restrict_field", "ptg_prolong_field", "ptg_restrict_data",
     "ptg_restrict_field_device", "ptg_prolong_field_device", "ptg_restrict_data_device",
     "ptg_halo_bytes", "ptg_halo_pack", "ptg_halo_unpack",
+    "ptg_comm_unique_id", "ptg_comm_init", "ptg_comm_destroy", "ptg_shard_layout", "ptg_plan_create_sharded",
+    "ptg_plan_bind_comm", "ptg_band_sync_halo",
     "ptg_solver_cfg_default", "ptg_mg_cfg_default", "ptg_driver_cfg_default",
     "ptg_metrics_device", "ptg_metrics_host", "ptg_canonical_phase",
     "ptg_lbfgs", "ptg_truncated_newton", "ptg_hier_create", "ptg_hier_destroy", "ptg_hier_level",
@@ -158,6 +161,13 @@ def lib() -> C.CDLL:
     L.ptg_restrict_field_device.argtypes = [C.c_int, _vp, C.c_int, _vp, _vp]
     L.ptg_prolong_field_device.argtypes = [C.c_int, _vp, C.c_int, _vp, _vp]
     L.ptg_restrict_data_device.argtypes = [C.c_int, _vp, C.c_int, C.c_int, _vp, _vp]
+    L.ptg_comm_unique_id.argtypes = [_vp]
+    L.ptg_comm_init.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]
+    L.ptg_comm_destroy.argtypes = [_vp]
+    L.ptg_shard_layout.argtypes = [C.c_int, C.c_int, C.c_int, _vp, C.c_int, C.c_int, C.c_int, _vp]
+    L.ptg_plan_create_sharded.argtypes = [C.POINTER(PlanDesc), C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]
+    L.ptg_plan_bind_comm.argtypes = [_vp, _vp]
+    L.ptg_band_sync_halo.argtypes = [_vp, _vp]
     L.ptg_halo_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
     L.ptg_halo_bytes.restype = C.c_size_t
     L.ptg_halo_pack.argtypes = [C.c_int, _vp, C.c_int, C.c_int, _vp, _vp, _vp]

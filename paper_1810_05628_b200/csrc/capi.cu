@@ -19,6 +19,9 @@
 struct ptg_plan {
     std::unique_ptr<ptg::Plan> p;
 };
+struct ptg_comm {
+    ptg::Comm* c = nullptr;
+};
 struct ptg_hier {
     std::unique_ptr<ptg::Hier> h;
     ptg_plan* fine;
@@ -49,6 +52,15 @@ ptg::Plan& P(ptg_plan* p) {
     if (!p || !p->p) ptg::raise(PTG_ERR_CONFIG, "objective is not bound to geometry/data (null plan)");
     PTG_CUDA(cudaSetDevice(p->p->device));
     return *p->p;
+}
+
+// the solvers / PIE / hierarchies need whole-object vectors on every rank
+ptg::Plan& P_whole(ptg_plan* p, const char* what) {
+    ptg::Plan& pl = P(p);
+    if (pl.shard.layout == PTG_SHARD_BANDS)
+        ptg::raise(PTG_ERR_CONFIG, std::string(what) + " on an object-band shard is not supported (evaluation only); "
+                                                       "use the replicated layout");
+    return pl;
 }
 
 void fill_report(ptg_report* rep, const ptg::Counter& c, double value, int reason, int hist_len) {
@@ -355,7 +367,7 @@ int ptg_pie_cb(ptg_plan* plan, double* z, double gamma, int sweeps, double max_w
                double* final_value, ptg_hist* hist, int hist_cap, int* hist_len, double* weighted,
                int* reason, ptg_iter_cb cb, void* user) {
     return guard([&] {
-        ptg::Plan& p = P(plan);
+        ptg::Plan& p = P_whole(plan, "pie");
         if (gamma < 0.0) ptg::raise(PTG_ERR_CONFIG, "pie: gamma must be non-negative");
         const size_t len = p.nn();
         ptg::DVec zd(p, len), gd(p, len);
@@ -496,7 +508,7 @@ int solve_ex(bool tn, ptg_plan* plan, int metric, const double* v, const double*
              const double* warm_grad, const ptg_solver_cfg* cfg, double* z_out, double* grad_out, ptg_report* rep,
              ptg_hist* hist, int hist_cap, ptg_iter_cb cb, void* user) {
     return guard([&] {
-        ptg::Plan& p = P(plan);
+        ptg::Plan& p = P_whole(plan, tn ? "truncatedNewton" : "lbfgs");
         ptg_solver_cfg c;
         if (cfg) c = *cfg;
         else ptg_solver_cfg_default(&c);
@@ -559,6 +571,65 @@ int ptg_fft2(const double* in, int n, int inverse, double* out) {
         PTG_CUDA(cudaMemcpy(a.p, in, bytes, cudaMemcpyHostToDevice));
         ptg::dev_fft2(a.p, n, inverse != 0, b.p, nullptr);
         PTG_CUDA(cudaMemcpy(out, b.p, bytes, cudaMemcpyDeviceToHost));
+    });
+}
+
+int ptg_comm_unique_id(unsigned char id[128]) {
+    return guard([&] {
+        if (!id) ptg::raise(PTG_ERR_CONFIG, "null id buffer");
+        ptg::comm_unique_id(id);
+    });
+}
+
+int ptg_comm_init(const unsigned char id[128], int world, int rank, int device, ptg_comm** out) {
+    return guard([&] {
+        if (!id || !out) ptg::raise(PTG_ERR_CONFIG, "null argument");
+        auto c = std::make_unique<ptg_comm>();
+        c->c = ptg::comm_init(id, world, rank, device);
+        *out = c.release();
+    });
+}
+
+int ptg_comm_destroy(ptg_comm* comm) {
+    return guard([&] {
+        if (!comm) return;
+        ptg::comm_destroy(comm->c);
+        delete comm;
+    });
+}
+
+int ptg_shard_layout(int n, int w, int N, const int32_t* positions, int world, int rank, int layout, int out[6]) {
+    return guard([&] {
+        if (!out || (N > 0 && !positions)) ptg::raise(PTG_ERR_CONFIG, "null argument");
+        ptg::shard_layout(n, w, N, positions, world, rank, layout, out);
+    });
+}
+
+int ptg_plan_create_sharded(const ptg_plan_desc* desc, int world, int rank, int layout, ptg_plan** out) {
+    return guard([&] {
+        if (!desc || !out) ptg::raise(PTG_ERR_CONFIG, "null argument");
+        auto h = std::make_unique<ptg_plan>();
+        h->p = ptg::plan_create_sharded(*desc, world, rank, layout);
+        *out = h.release();
+    });
+}
+
+int ptg_plan_bind_comm(ptg_plan* plan, ptg_comm* comm) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        if (!comm || !comm->c) ptg::raise(PTG_ERR_CONFIG, "null communicator");
+        if (p.shard.layout == PTG_SHARD_NONE) ptg::raise(PTG_ERR_CONFIG, "plan is not sharded (ptg_plan_create_sharded)");
+        if (ptg::comm_world(comm->c) != p.shard.world || ptg::comm_rank(comm->c) != p.shard.rank)
+            ptg::raise(PTG_ERR_CONFIG, "communicator rank / world size do not match the plan's shard");
+        p.comm = comm->c;
+    });
+}
+
+int ptg_band_sync_halo(ptg_plan* plan, void* z_dev) {
+    return guard([&] {
+        ptg::Plan& p = P(plan);
+        if (!z_dev) ptg::raise(PTG_ERR_CONFIG, "null iterate");
+        ptg::comm_sync_halo(p, z_dev);
     });
 }
 

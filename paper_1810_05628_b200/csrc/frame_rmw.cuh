@@ -343,9 +343,11 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
 }
 
 // grad = -v (MG/OPT shift) or 0, <v,z> partial per block, counters zeroed
+// (elements >= own: 0 and no <v,z> share -- a BANDS shard's halo rows, whose
+// contributions are added on the next rank)
 template <typename C>
 __global__ void __launch_bounds__(256) k_rmw_init(const C* __restrict__ v, const C* __restrict__ z,
-                                                  C* __restrict__ grad, size_t len, double* dotp,
+                                                  C* __restrict__ grad, size_t len, size_t own, double* dotp,
                                                   unsigned* done, int N, unsigned* work) {
     __shared__ double red[8];
     const size_t chunk = (len + gridDim.x - 1) / gridDim.x;
@@ -353,7 +355,7 @@ __global__ void __launch_bounds__(256) k_rmw_init(const C* __restrict__ v, const
     double d = 0.0;
     for (size_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
         C gv;
-        if (v) {
+        if (v && i < own) {
             const C vv = v[i], zz = z[i];
             gv.x = -vv.x;
             gv.y = -vv.y;

@@ -753,6 +753,15 @@ __global__ void __launch_bounds__(256) k_finalize(const double* __restrict__ mis
     finalize_block(misfit, N, dotp, ndot, out, red, threadIdx.x);
 }
 
+// value -= sum of the dot partials (fixed order; one thread)
+constexpr int kShiftBlocks = 1024;
+__global__ void k_sub_dots(const double* __restrict__ dotp, int ndot, double* value) {
+    if (threadIdx.x != 0) return;
+    double s = 0.0;
+    for (int i = 0; i < ndot; ++i) s += dotp[i];
+    *value -= s;
+}
+
 // --------------------------------------------------------------- data prep
 // d >= 0 check (checkPattern, objectives.cpp:12-18) + amp = sqrt(d)
 template <typename R>
@@ -1028,11 +1037,13 @@ void build_chunks(Plan& p) {
     p.tiles_y = (p.n + kTileH - 1) / kTileH;
     p.mp = !frame_single_cta(p.prec, p.M);
     p.cl = cl_path_ok(p);
-    p.planes_mode = choose_planes(p);
+    if (p.rows != p.n && !(p.cl && p.w == p.M))
+        raise(PTG_ERR_CONFIG, "object bands (sharded plans) need the complex64 cluster path: M = 128 / 256, w = M");
+    p.planes_mode = p.rows == p.n && choose_planes(p);
     // RMW overlap-add for the cluster path when the planes do not fit
     // (PTG_NO_RMW=1 selects the stash + gather path instead; read per plan)
     const bool no_rmw = getenv("PTG_NO_RMW") && getenv("PTG_NO_RMW")[0] == '1';
-    p.rmw_mode = !p.planes_mode && p.cl && p.w == p.M && p.N > 0 && !no_rmw;
+    p.rmw_mode = (!p.planes_mode && p.cl && p.w == p.M && p.N > 0 && !no_rmw) || (p.rows != p.n && p.N > 0);
     if (p.rmw_mode) {   // one chunk, no tile lists, no stash
         auto c = std::make_unique<Chunk>();
         c->first = 0;
@@ -1167,8 +1178,13 @@ static void keep_pool_memory(int device) {
     done[device] = true;
 }
 
-std::unique_ptr<Plan> plan_create(const ptg_plan_desc& d) {
+static std::unique_ptr<Plan> plan_create_rows(const ptg_plan_desc& d, int rows, const Shard& shard);
+
+std::unique_ptr<Plan> plan_create(const ptg_plan_desc& d) { return plan_create_rows(d, d.n, Shard{}); }
+
+static std::unique_ptr<Plan> plan_create_rows(const ptg_plan_desc& d, int rows, const Shard& shard) {
     if (d.n < 1) raise(PTG_ERR_GEOMETRY, "object side must be positive");
+    if (rows < 1 || rows > d.n) raise(PTG_ERR_GEOMETRY, "object band rows must be in [1, n]");
     if (!is_pow2(d.M))
         raise(PTG_ERR_GEOMETRY, "fft2: grid side must be a positive power of two, got " + std::to_string(d.M));
     if (d.w < 1 || d.w > d.M || d.w > d.n)
@@ -1178,7 +1194,7 @@ std::unique_ptr<Plan> plan_create(const ptg_plan_desc& d) {
     if (d.N > 0 && !d.positions) raise(PTG_ERR_CONFIG, "positions pointer is NULL");
     for (int k = 0; k < d.N; ++k) {
         const int r = d.positions[2 * k], c = d.positions[2 * k + 1];
-        if (r < 0 || c < 0 || r + d.w > d.n || c + d.w > d.n)
+        if (r < 0 || c < 0 || r + d.w > rows || c + d.w > d.n)
             raise(PTG_ERR_GEOMETRY, "probe window [" + std::to_string(r) + "," + std::to_string(c) +
                                         ")+" + std::to_string(d.w) + " does not fit an n=" +
                                         std::to_string(d.n) + " grid");
@@ -1189,6 +1205,8 @@ std::unique_ptr<Plan> plan_create(const ptg_plan_desc& d) {
 
     auto p = std::make_unique<Plan>();
     p->n = d.n;
+    p->rows = rows;
+    p->shard = shard;
     p->M = d.M;
     p->w = d.w;
     p->N = d.N;
@@ -1361,8 +1379,10 @@ static void eval_t(Plan& p, int metric, const void* z, const void* v, void* grad
             // init (grad = -v | 0, <v,z> partials, counters) -> persistent RMW
             // frames -> value; all on the plan's stream
             p.ev_begin(1);
+            // a BANDS shard owns its first own_rows rows: the shift and <v,z> there only
+            const size_t own = p.shard.layout == PTG_SHARD_BANDS ? (size_t)p.shard.own_rows * p.n : p.nn();
             k_rmw_init<C><<<kRmwInitBlocks, 256, 0, p.stream>>>(static_cast<const C*>(v), static_cast<const C*>(z),
-                                                                static_cast<C*>(grad), p.nn(),
+                                                                static_cast<C*>(grad), p.nn(), own,
                                                                 v ? p.dotp.as<double>() : nullptr,
                                                                 p.rmw_done.as<unsigned>(), p.N, p.rmw_work.as<unsigned>());
             PTG_CHECK_LAUNCH();
@@ -1478,8 +1498,110 @@ void plan_eval(Plan& p, int metric, const void* z, const void* v, void* grad, do
         grad = p.gbuf.p;
     }
     if (!value_dev) value_dev = p.value.as<double>();
-    if (p.prec == PTG_C64) eval_t<float>(p, metric, z, v, grad, value_dev);
-    else eval_t<double>(p, metric, z, v, grad, value_dev);
+    // REPLICATED shards: local frames without the shift, the sum over ranks,
+    // then the shift once (grad -= v, value -= <v,z>, identical on every rank)
+    const bool rep = p.comm && p.shard.layout == PTG_SHARD_REPLICATED;
+    const void* v_local = rep ? nullptr : v;
+    if (p.prec == PTG_C64) eval_t<float>(p, metric, z, v_local, grad, value_dev);
+    else eval_t<double>(p, metric, z, v_local, grad, value_dev);
+    if (!p.comm) return;
+    comm_exchange(p, grad, value_dev);
+    if (rep && v) {
+        p.dotp.ensure((size_t)kShiftBlocks * sizeof(double));
+        if (p.prec == PTG_C64)
+            k_shift<float><<<kShiftBlocks, 256, 0, p.stream>>>(static_cast<const float2*>(v), static_cast<const float2*>(z),
+                                                               static_cast<float2*>(grad), p.nn(), p.dotp.as<double>());
+        else
+            k_shift<double><<<kShiftBlocks, 256, 0, p.stream>>>(static_cast<const double2*>(v), static_cast<const double2*>(z),
+                                                                static_cast<double2*>(grad), p.nn(), p.dotp.as<double>());
+        PTG_CHECK_LAUNCH();
+        k_sub_dots<<<1, 256, 0, p.stream>>>(p.dotp.as<const double>(), kShiftBlocks, value_dev);
+        PTG_CHECK_LAUNCH();
+        p.launches += 2;
+    }
+}
+
+// ------------------------------------------------------------- sharding
+void shard_layout(int n, int w, int N, const int32_t* pos, int world, int rank, int layout, int out[6]) {
+    if (world < 1 || rank < 0 || rank >= world) raise(PTG_ERR_CONFIG, "shard: bad rank / world size");
+    if (layout != PTG_SHARD_REPLICATED && layout != PTG_SHARD_BANDS) raise(PTG_ERR_CONFIG, "shard: unknown layout");
+    // scan rows: a new row once the window row moved by >= w/8 (build_rmw's grouping)
+    const int gap = std::max(1, w / 8);
+    std::vector<int> row_start;
+    for (int i = 0; i < N; ++i)
+        if (i == 0 || pos[2 * i] - pos[2 * row_start.back()] >= gap)
+            row_start.push_back(i);
+    const int G = (int)row_start.size();
+    if (G < world) raise(PTG_ERR_CONFIG, "shard: more ranks (" + std::to_string(world) + ") than scan rows (" +
+                                             std::to_string(G) + ")");
+    // block b: scan rows [cut[b], cut[b+1]) with ~N / world positions each
+    std::vector<int> cut(world + 1, G);
+    cut[0] = 0;
+    for (int b = 1; b < world; ++b) {
+        const double target = (double)N * b / world;
+        int g = cut[b - 1] + 1;
+        while (g < G - (world - b) && row_start[g] < target) ++g;
+        cut[b] = g;
+    }
+    auto first = [&](int b) { return cut[b] < G ? row_start[cut[b]] : N; };
+    auto min_row = [&](int b) {
+        int m = n;
+        for (int i = first(b); i < first(b + 1); ++i) m = std::min(m, (int)pos[2 * i]);
+        return m;
+    };
+    auto max_end = [&](int b) {
+        int m = 0;
+        for (int i = first(b); i < first(b + 1); ++i) m = std::max(m, (int)pos[2 * i] + w);
+        return m;
+    };
+    std::vector<int> R(world + 1, n);
+    R[0] = 0;
+    for (int b = 1; b < world; ++b) R[b] = min_row(b);
+    for (int b = 0; b + 1 < world; ++b)
+        if (max_end(b) - w > R[b + 1])
+            raise(PTG_ERR_CONFIG, "shard: scan rows of consecutive ranks interleave (window rows not ordered)");
+    out[0] = first(rank);
+    out[1] = first(rank + 1);
+    if (layout == PTG_SHARD_REPLICATED) {
+        out[2] = 0;
+        out[3] = n;
+        out[4] = n;
+        out[5] = 0;
+        return;
+    }
+    auto band_end = [&](int b) { return std::min(n, std::max(R[b + 1], max_end(b))); };
+    for (int b = 0; b + 1 < world; ++b)
+        if (band_end(b) - R[b + 1] > R[b + 2] - R[b + 1])
+            raise(PTG_ERR_CONFIG, "shard: a rank's halo (" + std::to_string(band_end(b) - R[b + 1]) +
+                                      " rows) exceeds the next rank's own rows; use fewer ranks");
+    out[2] = R[rank];
+    out[3] = band_end(rank) - R[rank];
+    out[4] = R[rank + 1] - R[rank];
+    out[5] = rank > 0 ? band_end(rank - 1) - R[rank] : 0;
+}
+
+std::unique_ptr<Plan> plan_create_sharded(const ptg_plan_desc& d, int world, int rank, int layout) {
+    if (d.N > 0 && !d.positions) raise(PTG_ERR_CONFIG, "positions pointer is NULL");
+    int L[6];
+    shard_layout(d.n, d.w, d.N, d.positions, world, rank, layout, L);
+    Shard sh;
+    sh.layout = layout;
+    sh.world = world;
+    sh.rank = rank;
+    sh.pos_begin = L[0];
+    sh.pos_end = L[1];
+    sh.row0 = L[2];
+    sh.own_rows = L[4];
+    sh.halo_prev = L[5];
+    std::vector<int32_t> local((size_t)2 * (L[1] - L[0]));
+    for (int i = L[0]; i < L[1]; ++i) {
+        local[2 * (size_t)(i - L[0])] = d.positions[2 * (size_t)i] - L[2];
+        local[2 * (size_t)(i - L[0]) + 1] = d.positions[2 * (size_t)i + 1];
+    }
+    ptg_plan_desc ld = d;
+    ld.N = L[1] - L[0];
+    ld.positions = local.data();
+    return plan_create_rows(ld, L[3], sh);
 }
 
 // ------------------------------------------------------ banded host eval
@@ -1680,8 +1802,8 @@ static void eval_host_rmw(Plan& p, int metric, const double* z, double* value, d
         PTG_CUDA(cudaEventRecord(ev_in[b], sin[b & 1]));
     }
     // gradient = 0, completion counters zeroed (no shift on this path)
-    k_rmw_init<C><<<kRmwInitBlocks, 256, 0, p.stream>>>(nullptr, nullptr, gd, nn, nullptr, p.rmw_done.as<unsigned>(), N,
-                                                        p.rmw_work.as<unsigned>());
+    k_rmw_init<C><<<kRmwInitBlocks, 256, 0, p.stream>>>(nullptr, nullptr, gd, nn, nn, nullptr, p.rmw_done.as<unsigned>(),
+                                                        N, p.rmw_work.as<unsigned>());
     PTG_CHECK_LAUNCH();
     ++p.launches;
     FrameArgs<float> a = frame_args<float>(p, zd, data);
@@ -1738,14 +1860,15 @@ static bool host_pinned(const void* ptr) {
 void plan_eval_host(Plan& p, int metric, const double* z, const double* v, double* value, double* grad) {
     LaunchScope ls(p);
     plan_ensure(p, metric);
-    if (p.rmw_mode && !v && grad && !p.timing && !(getenv("PTG_NO_BANDED") && getenv("PTG_NO_BANDED")[0] == '1')) {
+    if (p.rmw_mode && !p.comm && !v && grad && !p.timing &&
+        !(getenv("PTG_NO_BANDED") && getenv("PTG_NO_BANDED")[0] == '1')) {
         eval_host_rmw(p, metric, z, value, grad);
         return;
     }
     static const bool off = getenv("PTG_NO_BANDED") && getenv("PTG_NO_BANDED")[0] == '1';   // A/B switch
     bool sorted = true;
     for (int j = 1; j < p.N && sorted; ++j) sorted = p.pos_h[2 * j] >= p.pos_h[2 * (j - 1)];
-    const bool banded = !off && grad && p.planes_mode && p.chunks.size() == 1 && !p.mp && !p.timing && sorted &&
+    const bool banded = !off && !p.comm && grad && p.planes_mode && p.chunks.size() == 1 && !p.mp && !p.timing && sorted &&
                         p.N > 0 && p.n >= 64;
     if (banded) {
         auto run = [&](bool capture) {

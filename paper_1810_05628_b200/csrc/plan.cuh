@@ -68,8 +68,26 @@ constexpr int kTileH = 8;
 constexpr int kHvalDoubles = 16;
 constexpr int kRmwInitBlocks = 1024;   // fixed grid of k_rmw_init => fixed <v,z> partition   // pinned host scalars per plan (never reallocated)
 
+struct Comm;   // comm.cu (NCCL)
+
+// Multi-GPU sharding of one problem (comm.cu, ptg_plan_create_sharded): this
+// rank's positions are the contiguous scan block [pos_begin, pos_end) of the
+// global scan; REPLICATED plans hold the whole object, BANDS plans object
+// rows [row0, row0 + rows) = own_rows rows of their own + the halo their
+// windows reach into the next rank's rows.
+struct Shard {
+    int layout = PTG_SHARD_NONE;
+    int world = 1, rank = 0;
+    int row0 = 0, own_rows = 0, halo_prev = 0;   // halo_prev: rows the previous rank's halo adds here
+    int pos_begin = 0, pos_end = 0;
+};
+
 struct Plan {
     int n = 0, M = 0, w = 0, N = 0, prec = PTG_C64, device = 0;
+    int rows = 0;                    // object rows held (n unless a BANDS shard)
+    Shard shard;
+    Comm* comm = nullptr;            // bound NCCL communicator (not owned)
+    DevMem halo_buf;
     bool has_probe = false;
     std::vector<int32_t> pos_h;      // N x 2
     std::vector<double> probe_h;     // M x M complex128 (empty if binary)
@@ -170,7 +188,7 @@ struct Plan {
     ~Plan();
     size_t celem() const { return prec == PTG_C64 ? 8 : 16; }
     size_t relem() const { return prec == PTG_C64 ? 4 : 8; }
-    size_t nn() const { return (size_t)n * n; }
+    size_t nn() const { return (size_t)rows * n; }   // object elements held (rows x n)
     size_t MM() const { return (size_t)M * M; }
     bool ref_mode() const { return !has_probe && M == n; }
     size_t device_bytes() const;
@@ -184,6 +202,18 @@ struct LaunchScope {
 };
 
 std::unique_ptr<Plan> plan_create(const ptg_plan_desc& d);
+// this rank's share of a global problem (layout PTG_SHARD_REPLICATED | BANDS)
+std::unique_ptr<Plan> plan_create_sharded(const ptg_plan_desc& global, int world, int rank, int layout);
+// the partition itself (host only): out = {pos_begin, pos_end, row0, rows, own_rows, halo_prev}
+void shard_layout(int n, int w, int N, const int32_t* positions, int world, int rank, int layout, int out[6]);
+// NCCL (comm.cu)
+void comm_unique_id(unsigned char out[128]);
+Comm* comm_init(const unsigned char id[128], int world, int rank, int device);
+void comm_destroy(Comm* c);
+int comm_world(const Comm* c);
+int comm_rank(const Comm* c);
+void comm_exchange(Plan& p, void* grad, double* value_dev);   // after the local frames
+void comm_sync_halo(Plan& p, void* z);                        // BANDS: z's halo rows from rank + 1
 // status 4 unless `device` is a usable sm_100 device (selects it)
 void check_device_public(int device);
 // coarse plan built on device from a fine one (patch-model coarsening)

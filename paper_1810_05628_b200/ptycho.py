@@ -76,6 +76,7 @@ class Plan:
     def __init__(self, n: int, M: int, w: int, positions, data=None, probe=None,
                  precision="c64", device: int = 0):
         self.n, self.M, self.w = int(n), int(M), int(w)
+        self.rows = self.n   # object rows held (a BANDS shard holds fewer)
         self.positions = np.ascontiguousarray(positions, dtype=np.int32).reshape(-1, 2)
         self.N = self.positions.shape[0]
         self.precision = _prec(precision)
@@ -96,6 +97,52 @@ class Plan:
         d.device = int(device)
         self._h = C.c_void_p()
         check(lib().ptg_plan_create(C.byref(d), C.byref(self._h)))
+
+    @classmethod
+    def sharded(cls, n: int, M: int, w: int, positions, world: int, rank: int, layout: str = "bands",
+                data=None, probe=None, precision="c64", device: int = 0) -> "Plan":
+        """This rank's plan of a global problem (ptg_plan_create_sharded).
+        positions: ALL N positions (global scan order); data: None or this
+        rank's own patterns.  layout "bands" (object rows [row0, row0 + rows))
+        or "replicated" (whole object)."""
+        lay = {"replicated": L.PTG_SHARD_REPLICATED, "bands": L.PTG_SHARD_BANDS}[layout]
+        self = cls.__new__(cls)
+        self.n, self.M, self.w = int(n), int(M), int(w)
+        allpos = np.ascontiguousarray(positions, dtype=np.int32).reshape(-1, 2)
+        info = shard_layout(n, w, allpos, world, rank, layout)
+        self.shard = info
+        self.rows = info["rows"]
+        self.positions = allpos[info["pos_begin"]:info["pos_end"]].copy()
+        self.positions[:, 0] -= info["row0"]
+        self.N = self.positions.shape[0]
+        self.precision = _prec(precision)
+        self.probe = None if probe is None else _c128(probe).reshape(self.M, self.M)
+        d = L.PlanDesc()
+        d.n, d.M, d.w, d.N = self.n, self.M, self.w, allpos.shape[0]
+        d.positions = allpos.ctypes.data_as(C.POINTER(C.c_int32))
+        d.probe = (self.probe.view(np.float64).ctypes.data_as(C.POINTER(C.c_double))
+                   if self.probe is not None else None)
+        data_arr = None
+        if data is not None:
+            data_arr = np.ascontiguousarray(data)
+            if data_arr.dtype not in (np.float32, np.float64):
+                data_arr = data_arr.astype(np.float64)
+            d.data = data_arr.ctypes.data
+            d.data_dtype = L.PTG_F32 if data_arr.dtype == np.float32 else L.PTG_F64
+        d.precision = self.precision
+        d.device = int(device)
+        self._h = C.c_void_p()
+        check(lib().ptg_plan_create_sharded(C.byref(d), int(world), int(rank), lay, C.byref(self._h)))
+        return self
+
+    def bind_comm(self, comm: "Comm"):
+        """Evaluations return the global value and this rank's gradient (NCCL inside libptg)."""
+        check(lib().ptg_plan_bind_comm(self._h, comm._h))
+        self._comm = comm   # keep the communicator alive with the plan
+
+    def sync_halo(self, z):
+        """BANDS: fill z's halo rows [own_rows, rows) from the next rank (device tensor)."""
+        check(lib().ptg_band_sync_halo(self._h, _vp(z)))
 
     # -- lifetime
     def close(self):
@@ -154,14 +201,14 @@ class Plan:
     # -- objectives (host complex128)
     def evaluate(self, z, v=None, metric: int = DISTANCE, want_grad: bool = True, out=None):
         """(value, gradient); ``out`` may be a preallocated (e.g. pinned) complex128 array."""
-        z = _c128(z).reshape(self.n, self.n)
-        v = None if v is None else _c128(v).reshape(self.n, self.n)
+        z = _c128(z).reshape(self.rows, self.n)
+        v = None if v is None else _c128(v).reshape(self.rows, self.n)
         if out is not None:
-            if out.dtype != np.complex128 or not out.flags.c_contiguous or out.size != self.n * self.n:
+            if out.dtype != np.complex128 or not out.flags.c_contiguous or out.size != self.rows * self.n:
                 raise ConfigError("out must be a contiguous complex128 array of n*n entries")
             g = out
         else:
-            g = np.empty((self.n, self.n), np.complex128) if want_grad else None
+            g = np.empty((self.rows, self.n), np.complex128) if want_grad else None
         val = C.c_double()
         check(lib().ptg_eval(self._h, metric, z.ctypes.data, _vp(v), C.byref(val), _vp(g)))
         return val.value, g
@@ -181,14 +228,14 @@ class Plan:
         return val.value if sync_value else None
 
     def project_modulus(self, z, k: int) -> np.ndarray:
-        z = _c128(z).reshape(self.n, self.n)
+        z = _c128(z).reshape(self.rows, self.n)
         out = np.empty((self.M, self.M), np.complex128)
         check(lib().ptg_project_modulus(self._h, z.ctypes.data, int(k), out.ctypes.data))
         return out
 
     def simulate(self, z, copy_out: bool = True) -> Optional[np.ndarray]:
         """d_j = |fft2(P o S_j z)|^2 on the GPU; becomes the plan's data."""
-        z = _c128(z).reshape(self.n, self.n)
+        z = _c128(z).reshape(self.rows, self.n)
         out = np.empty((self.N, self.M, self.M), np.float64) if copy_out else None
         check(lib().ptg_simulate(self._h, z.ctypes.data, _vp(out)))
         return out
@@ -346,6 +393,42 @@ def restrict_data(fine) -> np.ndarray:
     out = np.empty((N, M // 2, M // 2), np.float64)
     check(lib().ptg_restrict_data(d.ctypes.data, N, M, out.ctypes.data))
     return out
+
+
+def shard_layout(n: int, w: int, positions, world: int, rank: int, layout: str = "bands") -> dict:
+    """The partition of a global scan over `world` ranks (host only, ptg_shard_layout)."""
+    lay = {"replicated": L.PTG_SHARD_REPLICATED, "bands": L.PTG_SHARD_BANDS}[layout]
+    pos = np.ascontiguousarray(positions, dtype=np.int32).reshape(-1, 2)
+    out = np.zeros(6, np.int32)
+    check(lib().ptg_shard_layout(int(n), int(w), pos.shape[0], pos.ctypes.data, int(world), int(rank), lay,
+                                 out.ctypes.data))
+    keys = ("pos_begin", "pos_end", "row0", "rows", "own_rows", "halo_prev")
+    return {k: int(v) for k, v in zip(keys, out)}
+
+
+class Comm:
+    """An NCCL communicator inside libptg (one per process / GPU).  The
+    128-byte ncclUniqueId is made on rank 0 and broadcast with `broadcast`
+    (e.g. torch.distributed over any backend)."""
+
+    def __init__(self, world: int, rank: int, device: int, broadcast):
+        uid = np.zeros(128, np.uint8)
+        if rank == 0:
+            check(lib().ptg_comm_unique_id(uid.ctypes.data))
+        uid = np.ascontiguousarray(broadcast(uid), dtype=np.uint8)
+        self._h = C.c_void_p()
+        check(lib().ptg_comm_init(uid.ctypes.data, int(world), int(rank), int(device), C.byref(self._h)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ptg_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def device_count() -> int:
