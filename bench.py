@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip other configs / V-cycle / PIE / CPU legs")
     ap.add_argument("--dist-selftest", action="store_true",
                     help="run the multi-rank (NCCL) code path with one rank (1-GPU check)")
+    ap.add_argument("--layout", default=None, choices=["bands", "replicated"],
+                    help="strong-scaling layout (default: bands for complex64 M >= 128, else replicated)")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="multi-GPU layout: strong = scan rows split, object replicated, gradient allreduce; "
                          "weak = object bands + halo exchange")
@@ -364,26 +366,29 @@ class GpuProblem:
     """A configuration resident on this GPU: plan, device data (our forward
     operator + device Poisson noise), iterate / gradient buffers."""
 
-    def __init__(self, cfg, obj, probe, pos, stream, device, comm=None):
+    def __init__(self, cfg, obj, probe, pos, stream, device, plan=None):
         import torch
 
         from paper_1810_05628_b200 import Plan
         self.cfg = cfg
         self.stream = stream
         self.cdt = torch.complex64 if cfg.precision == "c64" else torch.complex128
-        self.plan = Plan(cfg.n, cfg.M, cfg.w, pos, None, probe, precision=cfg.precision, device=device)
+        self.plan = plan if plan is not None else Plan(cfg.n, cfg.M, cfg.w, pos, None, probe,
+                                                       precision=cfg.precision, device=device)
         self.plan.set_stream(stream.cuda_stream)
-        if comm is not None:
-            self.plan.bind_comm(comm)
-        # data: our GPU forward operator (forward.cpp:40-54 restated) + device Poisson noise
+        # data: our GPU forward operator (forward.cpp:40-54 restated) + device
+        # Poisson noise; `obj` holds the plan's object rows
         self.plan.simulate(obj, copy_out=False)
         if cfg.photons:
             self.plan.add_poisson(cfg.photons, seed=4)
-        self.z = torch.ones(cfg.n, cfg.n, dtype=self.cdt, device="cuda")
+        self.bands = getattr(self.plan, "shard", {}).get("rows", cfg.n) != cfg.n
+        self.z = torch.ones(self.plan.rows, cfg.n, dtype=self.cdt, device="cuda")
         self.grad = torch.empty_like(self.z)
         self.val = torch.zeros(4, dtype=torch.float64, device="cuda")
 
     def step(self):
+        if self.bands:
+            self.plan.sync_halo(self.z)   # the iterate's halo rows from the next rank (NCCL)
         self.plan.evaluate_device(self.z, self.grad, value_dev=self.val, sync_value=False)
 
     def close(self):
@@ -510,11 +515,15 @@ def run_ours(args):
 
     from paper_1810_05628_b200 import sharding, synth
 
+    from paper_1810_05628_b200 import Comm, Plan
+
     cfg = synth.CONFIGS[args.config]
     obj, probe, pos = synth.make_inputs(cfg)
     banded = multi and args.scaling == "weak"
     overlap = cfg.w - cfg.step if banded else 0
     comm = None
+    splan = None
+    layout = args.layout or ("bands" if (cfg.precision == "c64" and cfg.M >= 128) else "replicated")
     if banded:
         # rank r: the config's scan on rows [r (n - overlap), + n) of a tall object
         H = world * (cfg.n - overlap) + overlap
@@ -522,20 +531,30 @@ def run_ours(args):
         big = synth.make_object(H, cfg.sigma_obj)
         obj = np.ascontiguousarray(big[off:off + cfg.n, :cfg.n])
         del big
-        pos_shard = pos
+        Nr = cfg.N
+    elif multi:
+        # strong scaling of ONE problem: this rank's share (libptg's partition)
+        # and libptg's own NCCL communicator -- every evaluation ends with the
+        # library's exchange (BANDS: halo rows send/recv + scalar allreduce;
+        # REPLICATED: allreduce of gradient + value)
+        def bcast(a):
+            t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+            dist.broadcast(t, 0)
+            return t.cpu().numpy()
+        comm = Comm(world, rank, local, bcast)
+        splan = Plan.sharded(cfg.n, cfg.M, cfg.w, pos, world, rank, layout, probe=probe,
+                             precision=cfg.precision, device=local)
+        splan.bind_comm(comm)
+        r0, rows = splan.shard["row0"], splan.rows
+        obj = np.ascontiguousarray(obj[r0:r0 + rows])
+        Nr = splan.N
     else:
-        lo, hi = sharding.row_block(cfg.steps, world, rank)
-        pos_shard = pos[lo * cfg.steps:hi * cfg.steps]
-        if multi:
-            # libptg's own NCCL communicator: the plan's evaluation ends with ONE
-            # allreduce of [gradient | misfit] issued from inside the library
-            comm = sharding.LibComm(dist, local)
-    Nr = pos_shard.shape[0]
+        Nr = cfg.N
 
     # a real (non-legacy) stream shared by torch and libptg so CUDA events see our kernels
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    gp = GpuProblem(cfg, obj, probe, pos_shard, stream, local, comm=comm)
+    gp = GpuProblem(cfg, obj, probe, pos, stream, local, plan=splan)
     plan = gp.plan
     # L2 eviction between timed steps: READ 512 MiB (> 126 MB L2) so no dirty
     # lines are left whose write-back would land inside the timed kernels
@@ -578,8 +597,8 @@ def run_ours(args):
                   "attribution_loop_ms_per_step": t_attr_ms / max(args.steps, 1)}
 
     # ---- e2e through the public host API: pinned host z in, value + grad out
-    zh = torch.ones(cfg.n, cfg.n, dtype=torch.complex128).pin_memory().numpy()
-    gh = torch.empty(cfg.n, cfg.n, dtype=torch.complex128).pin_memory().numpy()
+    zh = torch.ones(plan.rows, cfg.n, dtype=torch.complex128).pin_memory().numpy()
+    gh = torch.empty(plan.rows, cfg.n, dtype=torch.complex128).pin_memory().numpy()
     h2d, d2h = zh.nbytes, gh.nbytes + 8
     e2e_steps = max(args.steps, 100 if cfg.n <= 1024 else 10)
     if not multi:
@@ -594,6 +613,22 @@ def run_ours(args):
         for _ in range(e2e_steps):
             plan.evaluate(zh, out=gh)
         e2e_s = time.perf_counter() - t0
+    elif comm is not None:
+        # the host API on every rank: its object rows in, the global value and
+        # its gradient rows out (libptg's exchange inside ptg_eval)
+        def e2e_step():
+            plan.evaluate(zh, out=gh)
+        for _ in range(3):   # a fixed count on every rank (collectives inside)
+            e2e_step()
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        e2e_s = time.perf_counter() - t0
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
     else:
         z128 = torch.empty(cfg.n, cfg.n, dtype=torch.complex128, device="cuda")
         g128 = torch.empty_like(z128)
@@ -697,10 +732,13 @@ def run_ours(args):
                            (f"{cfg.describe()} per GPU: {world} bands of a {world * (cfg.n - overlap) + overlap}x{cfg.n} "
                             f"object, consecutive bands sharing {overlap} rows (one continuous raster)"),
                            "global_batch": total_patterns, "patterns_per_rank": Nr,
-                           "parallelism": (f"object bands x{world}: halo rows + misfit all-gathered per evaluation"
+                           "parallelism": (f"weak: object bands x{world}, halo rows + misfit all-gathered per evaluation"
                                            if banded else
-                                           f"scan-row blocks x{world}, object replicated, libptg NCCL allreduce of "
-                                           "[gradient | misfit] per evaluation")
+                                           (f"scan-row blocks x{world}, object row bands (libptg BANDS: halo gradient "
+                                            "rows NCCL send/recv + scalar allreduce, iterate halo sync)"
+                                            if layout == "bands" else
+                                            f"scan-row blocks x{world}, object replicated (libptg REPLICATED: NCCL "
+                                            "allreduce of gradient + value)"))
                            if multi else "single GPU",
                            "l2": "flushed between timed steps (512 MiB read)"},
                 "roofline": roofline, "roofline_fp32": roofline_fp32, "roofline_hbm": roofline_hbm,

@@ -263,7 +263,7 @@ class Plan:
     # -- solvers
     def pie(self, z0, gamma: float = 0.0, sweeps: int = 1,
             max_weighted: float = float("inf")) -> SolverReport:
-        z = _c128(z0).reshape(self.n, self.n).copy()
+        z = _c128(z0).reshape(self.rows, self.n).copy()
         cap = sweeps + 2
         hist = (L.Hist * cap)()
         nh, rs = C.c_int(), C.c_int()
@@ -281,8 +281,8 @@ class Plan:
         lib().ptg_solver_cfg_default(C.byref(c))
         for k, val in cfg.items():
             setattr(c, k, val)
-        z0 = _c128(z0).reshape(self.n, self.n)
-        v = None if v is None else _c128(v).reshape(self.n, self.n)
+        z0 = _c128(z0).reshape(self.rows, self.n)
+        v = None if v is None else _c128(v).reshape(self.rows, self.n)
         z = np.empty_like(z0)
         g = np.empty_like(z0)
         cap = c.max_iters + 2
@@ -355,6 +355,7 @@ class Hierarchy:
         n, M, w, N = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         check(lib().ptg_plan_info(h, C.byref(n), C.byref(M), C.byref(w), C.byref(N), None, None))
         v.n, v.M, v.w, v.N = n.value, M.value, w.value, N.value
+        v.rows = v.n
         v.precision = self.plan.precision
         v._h = h
         v._view_of = self   # keep the hierarchy alive; never destroyed through the view
