@@ -35,7 +35,8 @@ def test_band_shards_simulated_ranks(oracle, monkeypatch, world, shift):
     import torch
 
     from paper_1810_05628_b200 import Plan
-    n, M, pos, probe, data, z, v = _problem(oracle, jitter=2 if world == 3 else 0)
+    # >= 5 scan rows (240 object rows) per rank: a 256-row window's halo must fit
+    n, M, pos, probe, data, z, v = _problem(oracle, steps=5 * world + 1, jitter=2 if world == 3 else 0)
     monkeypatch.setenv("PTG_NO_PLANES", "1")
     full = Plan(n, M, M, pos, data, probe, precision="c64")
     zt = torch.from_numpy(z.astype(np.complex64)).cuda()
@@ -90,7 +91,10 @@ def test_nccl_one_rank_equals_plain_plan(oracle, monkeypatch, layout):
     for vv in (None, v):
         want_v, want_g = plain.evaluate(z, vv)
         got_v, got_g = sh.evaluate(z, vv)
-        assert got_v == want_v and np.array_equal(got_g, want_g)
+        if vv is None or layout == "bands":
+            assert got_v == want_v and np.array_equal(got_g, want_g)
+        else:   # REPLICATED applies the shift after the sum over ranks: (sum - v) vs (-v + sum)
+            assert rel(got_v, want_v) <= 1e-12 and rel_l2(got_g, want_g) <= 1e-6
     zt = torch.from_numpy(z.astype(np.complex64)).cuda()
     gt = torch.empty_like(zt)
     torch.cuda.synchronize()
