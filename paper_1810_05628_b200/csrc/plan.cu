@@ -1008,6 +1008,26 @@ void build_rmw(Plan& p) {
         off[k + 1] = (int)dep.size();
         cells[(size_t)cy * G + cx].push_back(k);
     }
+    // transitive pruning: d is implied by a later dependency d' of k that
+    // itself depends on d (d' completes only after d did) -- a raster frame
+    // keeps a handful of its ~60 overlapping predecessors, so a frame polls a
+    // few completion counters (each acquire invalidates the SM's L1) instead
+    // of all of them
+    std::vector<int> poff(N + 1, 0), pdep;
+    pdep.reserve(dep.size() / 4 + 16);
+    for (int k = 0; k < N; ++k) {
+        const int* b = dep.data() + off[k];
+        const int* e = dep.data() + off[k + 1];
+        for (const int* it = b; it != e; ++it) {
+            bool implied = false;
+            for (const int* jt = it + 1; jt != e && !implied; ++jt)
+                implied = std::binary_search(dep.data() + off[*jt], dep.data() + off[*jt + 1], *it);
+            if (!implied) pdep.push_back(*it);
+        }
+        poff[k + 1] = (int)pdep.size();
+    }
+    off.swap(poff);
+    dep.swap(pdep);
     p.rmw_order_h = order;
     p.rmw_order.alloc(std::max<size_t>(1, (size_t)N) * sizeof(int));
     p.rmw_dep_off.alloc((size_t)(N + 1) * sizeof(int));
