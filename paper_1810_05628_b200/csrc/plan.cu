@@ -968,20 +968,37 @@ void build_rmw(Plan& p) {
     order.reserve(N);
     p.rmw_group_end.clear();
     p.rmw_group_maxr0.clear();
-    const int gap = std::max(1, w / 8);
+    // groups span `sb` window rows (PTG_RMW_SB, default 4 w): a frame waits
+    // for its overlapping predecessors, and these are a whole colour class of
+    // the group (~ frames per group / colours) earlier in the order, which
+    // must exceed the frames in flight (one per cluster) for the wait to be
+    // free; the group's gradient rows (sb + w) x n stay L2-resident
+    const char* esb = getenv("PTG_RMW_SB");
+    const int gap = std::max(1, esb ? atoi(esb) : 4 * w);
     for (int s = 0; s < N;) {
         int e = s + 1;
         while (e < N && r0(idx[e]) - r0(idx[s]) < gap) ++e;
+        // greedy colouring of the group through a grid of w x w cells
         std::vector<int> col(e - s, 0);
         int ncol = 0;
-        for (int i = s; i < e; ++i) {
-            std::vector<char> used(ncol + 1, 0);
-            for (int i2 = s; i2 < i; ++i2)
-                if (overlap(idx[i], idx[i2])) used[col[i2 - s]] = 1;
-            int c = 0;
-            while (used[c]) ++c;
-            col[i - s] = c;
-            ncol = std::max(ncol, c + 1);
+        {
+            const int Gc = std::max(1, (p.n + w - 1) / w);
+            const int rbase = r0(idx[s]) / w;
+            const int Gr = (r0(idx[e - 1]) / w) - rbase + 1;
+            std::vector<std::vector<int>> cell((size_t)Gr * Gc);
+            for (int i = s; i < e; ++i) {
+                const int cy = r0(idx[i]) / w - rbase, cx = std::min(c0(idx[i]) / w, Gc - 1);
+                std::vector<char> used(ncol + 1, 0);
+                for (int yy = std::max(0, cy - 1); yy <= std::min(Gr - 1, cy + 1); ++yy)
+                    for (int xx = std::max(0, cx - 1); xx <= std::min(Gc - 1, cx + 1); ++xx)
+                        for (int i2 : cell[(size_t)yy * Gc + xx])
+                            if (overlap(idx[i], idx[i2])) used[col[i2 - s]] = 1;
+                int c = 0;
+                while (c < (int)used.size() && used[c]) ++c;
+                col[i - s] = c;
+                ncol = std::max(ncol, c + 1);
+                cell[(size_t)cy * Gc + cx].push_back(i);
+            }
         }
         for (int c = 0; c < ncol; ++c)
             for (int i = s; i < e; ++i)
@@ -1063,7 +1080,15 @@ void build_chunks(Plan& p) {
     // RMW overlap-add for the cluster path when the planes do not fit
     // (PTG_NO_RMW=1 selects the stash + gather path instead; read per plan)
     const bool no_rmw = getenv("PTG_NO_RMW") && getenv("PTG_NO_RMW")[0] == '1';
-    p.rmw_mode = (!p.planes_mode && p.cl && p.w == p.M && p.N > 0 && !no_rmw) || (p.rows != p.n && p.N > 0);
+    // (the RMW order needs many more frames per colour class than clusters in
+    // flight: problems whose stash fits one chunk (configs 3-4) keep the
+    // stash + gather path; PTG_RMW=1 forces RMW)
+    const bool force_rmw = getenv("PTG_RMW") && getenv("PTG_RMW")[0] == '1';
+    const size_t stash_bytes = (size_t)p.N * p.w * stash_pitch(p.w) * p.celem();
+    size_t budget_b = (size_t)2 << 30;
+    if (const char* e = getenv("PTG_STASH_BUDGET_MB")) budget_b = std::max<size_t>(1, (size_t)atoll(e)) << 20;
+    p.rmw_mode = (!p.planes_mode && p.cl && p.w == p.M && p.N > 0 && !no_rmw && (force_rmw || stash_bytes > budget_b)) ||
+                 (p.rows != p.n && p.N > 0);
     if (p.rmw_mode) {   // one chunk, no tile lists, no stash
         auto c = std::make_unique<Chunk>();
         c->first = 0;

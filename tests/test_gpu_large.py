@@ -176,6 +176,7 @@ def test_rmw_matches_oracle(oracle, monkeypatch, M, steps, step, jitter, metric)
     v = _r64(0.01 * rand_field(n, 8))
     prob = oracle.Problem(n, M, M, pos, data.astype(np.float64), probe, metric)
     monkeypatch.setenv("PTG_NO_PLANES", "1")
+    monkeypatch.setenv("PTG_RMW", "1")
     plan = Plan(n, M, M, pos, data, probe, precision="c64")
     for vv in (v, None):
         gv, gg = plan.evaluate(z, vv, metric=metric)
@@ -196,7 +197,9 @@ def test_rmw_matches_stash_path(oracle, monkeypatch):
     cfg = synth.CONFIGS[3]
     prob, z, v, data, probe, pos, n = _case(oracle, cfg)
     monkeypatch.setenv("PTG_NO_PLANES", "1")
+    monkeypatch.setenv("PTG_RMW", "1")
     a = Plan(n, cfg.M, cfg.w, pos, data, probe, precision="c64")
+    monkeypatch.delenv("PTG_RMW")
     monkeypatch.setenv("PTG_NO_RMW", "1")
     b = Plan(n, cfg.M, cfg.w, pos, data, probe, precision="c64")
     va, ga = a.evaluate(z, v)
@@ -221,6 +224,7 @@ def test_rmw_banded_host_eval_bitwise(oracle, monkeypatch, bands):
     data = oracle.simulate(n, M, M, pos, obj, probe).astype(np.float32)
     z = _r64(obj * 0.9 + 0.05 * rand_field(n, 7))
     monkeypatch.setenv("PTG_NO_PLANES", "1")
+    monkeypatch.setenv("PTG_RMW", "1")
     monkeypatch.setenv("PTG_RMW_BANDS", bands)
     plan = Plan(n, M, M, pos, data, probe, precision="c64")
     hv, hg = plan.evaluate(z)

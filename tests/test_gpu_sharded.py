@@ -38,6 +38,7 @@ def test_band_shards_simulated_ranks(oracle, monkeypatch, world, shift):
     # >= 5 scan rows (240 object rows) per rank: a 256-row window's halo must fit
     n, M, pos, probe, data, z, v = _problem(oracle, steps=5 * world + 1, jitter=2 if world == 3 else 0)
     monkeypatch.setenv("PTG_NO_PLANES", "1")
+    monkeypatch.setenv("PTG_RMW", "1")
     full = Plan(n, M, M, pos, data, probe, precision="c64")
     zt = torch.from_numpy(z.astype(np.complex64)).cuda()
     vt = torch.from_numpy(v.astype(np.complex64)).cuda() if shift else None
@@ -84,6 +85,7 @@ def test_nccl_one_rank_equals_plain_plan(oracle, monkeypatch, layout):
     from paper_1810_05628_b200 import Comm, Plan
     n, M, pos, probe, data, z, v = _problem(oracle, steps=6)
     monkeypatch.setenv("PTG_NO_PLANES", "1")
+    monkeypatch.setenv("PTG_RMW", "1")
     plain = Plan(n, M, M, pos, data, probe, precision="c64")
     comm = Comm(1, 0, 0, _bcast_identity)
     sh = Plan.sharded(n, M, M, pos, 1, 0, layout, data=data, probe=probe, precision="c64")
