@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
     float* amp_s = reinterpret_cast<float*>(tw + M);     // [L][AP]
     __shared__ double red[NT / 32];
     __shared__ __align__(8) unsigned long long bar_a, bar_g;
-    __shared__ int s_item[2];   // the item of frames with even / odd index (written remotely by rank 0)
+    __shared__ int s_item;
 
     const int q = (int)cl.block_rank();
     const int t = threadIdx.x;
@@ -93,39 +93,29 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         fence_mbarrier_init();
     }
     for (int i = t; i < M; i += NT) tw[i] = __ldg(tw_g + i);
+    int next = 0;
+    if (q == 0 && t == 0) next = (int)atomicAdd(r.work, 1u);
     __syncthreads();
     const int m = t % L, g = t / L;
     const int rr = t % L, qq = t / L;
     const uint32_t bar_g_u = smem_u32(&bar_g), buf_u = smem_u32(buf);
-    uint32_t ph = 0, par = 0;
-    // Frame hand-off.  The item of frame f + 1 is published by rank 0 during
-    // frame f (into s_item[(f + 1) & 1] of every CTA, before frame f's full
-    // cluster barrier), and the barrier that keeps a frame's gather pushes
-    // out of a CTA that is still reading its rows is SPLIT: each CTA arrives
-    // when its epilogue is done and waits only right before its first push
-    // -- the amplitude copy and the first gather loads of the next frame are
-    // in flight meanwhile.
-    int next = 0;
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");   // every CTA's barriers initialised
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-    if (q == 0 && t == 0) {
-        const unsigned first = atomicAdd(r.work, 1u);
-        next = (int)atomicAdd(r.work, 1u);   // frame 1's item, claimed ahead
-#pragma unroll
-        for (int s = 0; s < Q; ++s) st_cluster_u32(mapa_u32(smem_u32(&s_item[0]), s), first);
-    }
-    if (t == 0) mbar_arrive_expect_tx(&bar_g, (uint32_t)(L * M * sizeof(float2)));   // frame 0's gather bytes
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");   // s_item[0] + expect_tx published
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");   // "rows free" for frame 0
+    uint32_t ph = 0;
 
 #pragma unroll 1
     for (;;) {
-        const int k = r.kbeg + s_item[par];
-        if (k >= r.kend) {
-            asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // the pending arrival
-            break;
+        // this frame's gather bytes, then the item handed to every CTA of the
+        // cluster; the full cluster barrier also orders every CTA's previous
+        // epilogue (reads of its own rows) before the pushes of this frame
+        if (t == 0) mbar_arrive_expect_tx(&bar_g, (uint32_t)(L * M * sizeof(float2)));
+        if (q == 0 && t == 0) {
+#pragma unroll
+            for (int s = 0; s < Q; ++s) st_cluster_u32(mapa_u32(smem_u32(&s_item), s), (unsigned)next);
+            next = (int)atomicAdd(r.work, 1u);   // the following frame, claimed ahead
         }
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        const int k = r.kbeg + s_item;
+        if (k >= r.kend) break;
         const int j = __ldg(r.order + k);
         const int2 pj = a.pos[j];
 
@@ -153,9 +143,6 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                         zv[i * Q + s] = zc[(size_t)row * n];
                         if constexpr (PROBE) pv[i * Q + s] = __ldg(a.probe + (size_t)row * M + t);
                     }
-                // every CTA has released its rows (its previous epilogue is done):
-                // needed only before the first remote push
-                if (b == 0) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 #pragma unroll
                 for (int i = 0; i < BT; ++i) {
                     const int rw = q * NPC + b + i;
@@ -269,11 +256,6 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
 #pragma unroll
                 for (int s = 0; s < Q; ++s) x[i * Q + s] = __ldg(probe_epi + (size_t)(q * NPC + i + L * s) * M + t);
         }
-        if (q == 0 && t == 0) {   // the next frame's item, published by the barrier below
-#pragma unroll
-            for (int s = 0; s < Q; ++s) st_cluster_u32(mapa_u32(smem_u32(&s_item[par ^ 1u]), s), (unsigned)next);
-            next = (int)atomicAdd(r.work, 1u);
-        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if ((t & 31) == 0) red[t / 32] = acc;
@@ -353,17 +335,10 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                 }
             }
         }
-        // (D) publish: this CTA's rows of frame k are final; then this CTA's
-        //     buffer is free for the next frame's pushes (its gather bytes
-        //     are expected first)
+        // (D) publish: this CTA's rows of frame k are final
         __syncthreads();
-        if (t == 0) {
-            red_release_gpu_add(r.done + k, 1u);
-            mbar_arrive_expect_tx(&bar_g, (uint32_t)(L * M * sizeof(float2)));
-        }
-        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        if (t == 0) red_release_gpu_add(r.done + k, 1u);
         ph ^= 1u;
-        par ^= 1u;
     }
 }
 

@@ -968,13 +968,13 @@ void build_rmw(Plan& p) {
     order.reserve(N);
     p.rmw_group_end.clear();
     p.rmw_group_maxr0.clear();
-    // groups span `sb` window rows (PTG_RMW_SB, default 4 w): a frame waits
-    // for its overlapping predecessors, and these are a whole colour class of
-    // the group (~ frames per group / colours) earlier in the order, which
-    // must exceed the frames in flight (one per cluster) for the wait to be
-    // free; the group's gradient rows (sb + w) x n stay L2-resident
+    // groups: window rows within PTG_RMW_SB (default w / 8: one scan row of a
+    // raster).  Measured on config 5 (ms per evaluation): w/8 24.5, 2 w 25.6,
+    // 4 w 26.9, 6 w 27.0 -- larger colour classes give the dependency waits
+    // more slack but scatter consecutive frames over more object rows (z and
+    // gradient locality in L2), which costs more than the waits
     const char* esb = getenv("PTG_RMW_SB");
-    const int gap = std::max(1, esb ? atoi(esb) : 4 * w);
+    const int gap = std::max(1, esb ? atoi(esb) : w / 8);
     for (int s = 0; s < N;) {
         int e = s + 1;
         while (e < N && r0(idx[e]) - r0(idx[s]) < gap) ++e;
