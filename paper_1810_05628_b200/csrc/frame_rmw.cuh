@@ -68,6 +68,21 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
     return make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 
+#ifdef ABL_TIMELINE   // diagnostic build: per-frame phase stamps of the first 64 CTAs (tools/rmw_timeline.py)
+constexpr int kRtlCtas = 64, kRtlFrames = 128, kRtlStamps = 12;
+__device__ unsigned long long g_rmw_tl[kRtlCtas * kRtlFrames * kRtlStamps];
+#define RTL(k)                                                                                   \
+    do {                                                                                         \
+        if (threadIdx.x == 0 && blockIdx.x < kRtlCtas && rtl_f < kRtlFrames) {                   \
+            unsigned long long t_;                                                               \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                               \
+            g_rmw_tl[((size_t)blockIdx.x * kRtlFrames + rtl_f) * kRtlStamps + (k)] = t_;          \
+        }                                                                                        \
+    } while (0)
+#else
+#define RTL(k)
+#endif
+
 template <int Q, int L, int OP, bool PROBE>
 __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
     frame_rmw_kernel(FrameArgs<float> a, const float* __restrict__ amp_perm, const float2* __restrict__ tw_g,
@@ -101,8 +116,12 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
     const uint32_t bar_g_u = smem_u32(&bar_g), buf_u = smem_u32(buf);
     uint32_t ph = 0;
 
+#ifdef ABL_TIMELINE
+    int rtl_f = 0;
+#endif
 #pragma unroll 1
     for (;;) {
+        RTL(0);
         // this frame's gather bytes, then the item handed to every CTA of the
         // cluster; the full cluster barrier also orders every CTA's previous
         // epilogue (reads of its own rows) before the pushes of this frame
@@ -116,6 +135,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         const int k = r.kbeg + s_item;
         if (k >= r.kend) break;
+        RTL(1);
         const int j = __ldg(r.order + k);
         const int2 pj = a.pos[j];
 
@@ -158,7 +178,9 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                 }
             }
         }
+        RTL(2);
         mbar_wait(&bar_g, ph);   // all Q senders' rows have landed in this CTA
+        RTL(3);
 
         double acc = 0.0;
 #pragma unroll 1
@@ -176,6 +198,9 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                 }
             }
             reg_fft<L, false>(x);
+#ifdef ABL_TIMELINE
+            if (pass == 1) RTL(4);
+#endif
             if (pass == 0) {
 #pragma unroll
                 for (int kk = 0; kk < L; ++kk) buf[kk * PM + t] = x[kk];
@@ -222,6 +247,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                     }
                 }
                 acc = ((double)af[0] + (double)af[1]) + ((double)af[2] + (double)af[3]);
+                RTL(5);
             } else if (pass == 2) {
 #pragma unroll
                 for (int c = 0; c < L; c += 2)
@@ -241,6 +267,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                     for (int s = 0; s < Q; ++s) row[L * s] = v[s];
                 }
                 __syncthreads();
+                RTL(6);
             } else {
                 asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 #pragma unroll
@@ -259,7 +286,9 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if ((t & 31) == 0) red[t / 32] = acc;
+        RTL(7);
         cl.sync();   // every push has landed; no remote access to this CTA's rows until the next frame
+        RTL(8);
         if (t == 0) {
             double s = 0.0;
 #pragma unroll
@@ -285,6 +314,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
             for (int s = 0; s < Q; ++s)
                 buf[(i * Q + s) * PM + t] = PROBE ? epi_contrib_pre(v[s], x[i * Q + s]) : epi_contrib(v[s], sc);
         }
+        RTL(9);
         // (B) every earlier overlapping frame has finished its update
         {
             const int d0 = __ldg(r.dep_off + k), d1 = __ldg(r.dep_off + k + 1);
@@ -294,6 +324,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
             }
         }
         __syncthreads();
+        RTL(10);
         // (C) read-modify-write of this CTA's L object rows, coalesced; every
         //     load in flight at once (x[] is free again)
         float2* G0 = r.grad + (size_t)pj.x * n + pj.y;
@@ -338,6 +369,10 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         // (D) publish: this CTA's rows of frame k are final
         __syncthreads();
         if (t == 0) red_release_gpu_add(r.done + k, 1u);
+        RTL(11);
+#ifdef ABL_TIMELINE
+        ++rtl_f;
+#endif
         ph ^= 1u;
     }
 }

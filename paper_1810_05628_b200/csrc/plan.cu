@@ -2253,4 +2253,7 @@ double plan_dot(Plan& p, const void* a, const void* b, size_t len) {
 extern "C" int ptg_debug_timeline(void* dst, size_t bytes) {
     return (int)cudaMemcpyFromSymbol(dst, ptg::g_tl, bytes < sizeof(ptg::g_tl) ? bytes : sizeof(ptg::g_tl));
 }
+extern "C" int ptg_debug_rmw_timeline(void* dst, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(dst, ptg::g_rmw_tl, bytes < sizeof(ptg::g_rmw_tl) ? bytes : sizeof(ptg::g_rmw_tl));
+}
 #endif
