@@ -147,35 +147,46 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                 tma_bulk_g2s(amp_s + r2 * AP, src + (size_t)r2 * M, M * sizeof(float), &bar_a);
         }
 
-        // gather fused with the column DIF butterflies (frame_cl.cuh)
+        // gather fused with the column DIF butterflies (frame_cl.cuh): the NPC
+        // butterfly rows of this CTA, software-pipelined two deep (the loads
+        // of butterfly b + 2 are issued as soon as b's registers are consumed)
         float2 x[L];
         {
-            constexpr int BT = 16 / Q;
             const float2* zc = a.z + (size_t)pj.x * n + pj.y + t;
-#pragma unroll 1
-            for (int b = 0; b < NPC; b += BT) {
-                float2 zv[BT * Q], pv[BT * Q];
+            float2 zb[2][Q], pb[2][Q];
+            const size_t zstep = (size_t)L * n;
+            auto load = [&](int b, int u) {
+                // rows q NPC + b + L s through running pointers (one live
+                // address per stream); volatile loads keep program order --
+                // the compiler would otherwise hoist every butterfly's loads
+                const float2* zp = zc + (size_t)(q * NPC + b) * n;
+                const float2* pp = a.probe + (size_t)(q * NPC + b) * M + t;
 #pragma unroll
-                for (int i = 0; i < BT; ++i)
-#pragma unroll
-                    for (int s = 0; s < Q; ++s) {
-                        const int row = q * NPC + b + i + L * s;
-                        zv[i * Q + s] = zc[(size_t)row * n];
-                        if constexpr (PROBE) pv[i * Q + s] = __ldg(a.probe + (size_t)row * M + t);
+                for (int s = 0; s < Q; ++s) {
+                    zb[u][s] = ldg_pinned(zp);
+                    zp += zstep;
+                    if constexpr (PROBE) {
+                        pb[u][s] = ldg_pinned(pp);
+                        pp += (size_t)L * M;
                     }
-#pragma unroll
-                for (int i = 0; i < BT; ++i) {
-                    const int rw = q * NPC + b + i;
-                    float2 v[Q];
-#pragma unroll
-                    for (int s = 0; s < Q; ++s) v[s] = PROBE ? cmul(pv[i * Q + s], zv[i * Q + s]) : zv[i * Q + s];
-                    dft_q<Q>(v);
-#pragma unroll
-                    for (int s = 1; s < Q; ++s) v[s] = cmul(tw[rw * s], v[s]);
-#pragma unroll
-                    for (int s = 0; s < Q; ++s)
-                        st_async_f2(mapa_u32(smem_u32(buf + rw * PM + t), s), v[s], mapa_u32(bar_g_u, s));
                 }
+            };
+            load(0, 0);
+            if constexpr (NPC > 1) load(1, 1);
+#pragma unroll
+            for (int b = 0; b < NPC; ++b) {
+                const int u = b & 1;
+                const int rw = q * NPC + b;
+                float2 v[Q];
+#pragma unroll
+                for (int s = 0; s < Q; ++s) v[s] = PROBE ? cmul(pb[u][s], zb[u][s]) : zb[u][s];
+                if (b + 2 < NPC) load(b + 2, u);
+                dft_q<Q>(v);
+#pragma unroll
+                for (int s = 1; s < Q; ++s) v[s] = cmul(tw[rw * s], v[s]);
+#pragma unroll
+                for (int s = 0; s < Q; ++s)
+                    st_async_f2(mapa_u32(smem_u32(buf + rw * PM + t), s), v[s], mapa_u32(bar_g_u, s));
             }
         }
         RTL(2);
@@ -348,9 +359,9 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                 }
             }
         } else {
-            constexpr int PER = L * M / NT, HALF = PER / 2;
+            constexpr int PER = L * M / NT, HALF = PER / 4;   // four batches of float2 (cold path)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < 4; ++h) {
                 float2 gv[HALF];
 #pragma unroll
                 for (int u = 0; u < HALF; ++u) {
