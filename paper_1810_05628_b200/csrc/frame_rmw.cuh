@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
     float* amp_s = reinterpret_cast<float*>(tw + M);     // [L][AP]
     __shared__ double red[NT / 32];
     __shared__ __align__(8) unsigned long long bar_a, bar_g;
-    __shared__ int s_item;
+    __shared__ int4 s_item;   // (order index k, position j, window row, window column) of this frame
 
     const int q = (int)cl.block_rank();
     const int t = threadIdx.x;
@@ -108,8 +108,22 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         fence_mbarrier_init();
     }
     for (int i = t; i < M; i += NT) tw[i] = __ldg(tw_g + i);
-    int next = 0;
-    if (q == 0 && t == 0) next = (int)atomicAdd(r.work, 1u);
+    // Rank 0 (thread 0) claims the next frame one frame ahead and fetches its
+    // position index and window: three dependent L2 round trips, spread over
+    // the current frame's phases (claim at the loop top, index after the
+    // gather, window after the spectral pass) so no warp waits on them; the
+    // loop top hands all four values to every CTA.
+    const bool leader = q == 0 && t == 0;
+    int4 next = make_int4(0, 0, 0, 0);
+    if (leader) {
+        next.x = r.kbeg + (int)atomicAdd(r.work, 1u);
+        if (next.x < r.kend) {
+            next.y = __ldg(r.order + next.x);
+            const int2 pp = a.pos[next.y];
+            next.z = pp.x;
+            next.w = pp.y;
+        }
+    }
     __syncthreads();
     const int m = t % L, g = t / L;
     const int rr = t % L, qq = t / L;
@@ -128,16 +142,23 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         if (t == 0) mbar_arrive_expect_tx(&bar_g, (uint32_t)(L * M * sizeof(float2)));
         if (q == 0 && t == 0) {
 #pragma unroll
-            for (int s = 0; s < Q; ++s) st_cluster_u32(mapa_u32(smem_u32(&s_item), s), (unsigned)next);
-            next = (int)atomicAdd(r.work, 1u);   // the following frame, claimed ahead
+            for (int s = 0; s < Q; ++s) {
+                const uint32_t base = mapa_u32(smem_u32(&s_item), s);
+                st_cluster_u32(base, (unsigned)next.x);
+                st_cluster_u32(base + 4, (unsigned)next.y);
+                st_cluster_u32(base + 8, (unsigned)next.z);
+                st_cluster_u32(base + 12, (unsigned)next.w);
+            }
+            next.x = r.kbeg + (int)atomicAdd(r.work, 1u);   // the following frame, claimed ahead
         }
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-        const int k = r.kbeg + s_item;
+        const int4 it = s_item;
+        const int k = it.x;
         if (k >= r.kend) break;
         RTL(1);
-        const int j = __ldg(r.order + k);
-        const int2 pj = a.pos[j];
+        const int j = it.y;
+        const int2 pj = make_int2(it.z, it.w);
 
         if (t < 32) {   // this CTA's L permuted amplitude rows, one bulk copy per row
             const float* src = amp_perm + (size_t)j * M * M + (size_t)q * L * M;
@@ -189,6 +210,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                     st_async_f2(mapa_u32(smem_u32(buf + rw * PM + t), s), v[s], mapa_u32(bar_g_u, s));
             }
         }
+        if (leader && next.x < r.kend) next.y = __ldg(r.order + next.x);
         RTL(2);
         mbar_wait(&bar_g, ph);   // all Q senders' rows have landed in this CTA
         RTL(3);
@@ -258,6 +280,11 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                     }
                 }
                 acc = ((double)af[0] + (double)af[1]) + ((double)af[2] + (double)af[3]);
+                if (leader && next.x < r.kend) {
+                    const int2 pp = a.pos[next.y];
+                    next.z = pp.x;
+                    next.w = pp.y;
+                }
                 RTL(5);
             } else if (pass == 2) {
 #pragma unroll
