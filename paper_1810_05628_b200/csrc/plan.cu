@@ -22,6 +22,7 @@
 
 #include "frame_cl.cuh"
 #include "frame_rmw.cuh"
+#include "frame_rmw2.cuh"
 #include "frame_kernels.cuh"
 #include "frame_multipass.cuh"
 #include "frame_tma.cuh"
@@ -281,6 +282,13 @@ int cl_line(const Plan& p) {
     static const int env = getenv("PTG_CL_L") ? atoi(getenv("PTG_CL_L")) : 0;
     return env == 64 ? 64 : 32;
 }
+constexpr int kSplitLine = 33;   // cl_amp tag: the split (two threads per line) order of frame_rmw2_kernel
+// M = 256 RMW plans use frame_rmw2_kernel (512 threads, two per line) unless PTG_RMW2=0
+bool rmw2(const Plan& p) {
+    if (p.M != 256) return false;
+    const char* e = getenv("PTG_RMW2");
+    return !(e && e[0] == '0');
+}
 // local line of the persistent RMW kernel: 8-CTA (M = 256) / 4-CTA (M = 128)
 // clusters of 32-row CTAs.  Measured and rejected: 16-CTA clusters of 16-row
 // CTAs at 3 per SM (M = 256): 27.9 vs 22.5 ms per config-5 evaluation (more
@@ -301,8 +309,16 @@ const float* cl_amp(Plan& p, const float* data, int L) {
     if (p.amp_cl_src != data || p.amp_cl_gen != p.data_gen || p.amp_cl_line != L) {
         const size_t total = (size_t)p.N * p.MM();
         p.amp_cl.ensure(total * sizeof(float));
-        if (p.M == 128) L == 32 ? perm_amp<4, 32>(p, data, total) : perm_amp<2, 64>(p, data, total);
-        else L == 32 ? perm_amp<8, 32>(p, data, total) : perm_amp<4, 64>(p, data, total);
+        if (L == kSplitLine) {   // frame_rmw2_kernel's order (M = 256)
+            const int grid = (int)std::min<size_t>(148 * 16, (total + 255) / 256);
+            k_perm_amp_split<<<grid, 256, 0, p.stream>>>(data, p.amp_cl.as<float>(), total);
+            PTG_CHECK_LAUNCH();
+            ++p.launches;
+        } else if (p.M == 128) {
+            L == 32 ? perm_amp<4, 32>(p, data, total) : perm_amp<2, 64>(p, data, total);
+        } else {
+            L == 32 ? perm_amp<8, 32>(p, data, total) : perm_amp<4, 64>(p, data, total);
+        }
         p.amp_cl_src = data;
         p.amp_cl_gen = p.data_gen;
         p.amp_cl_line = L;
@@ -396,9 +412,50 @@ void launch_rmw_t(Plan& p, const FrameArgs<float>& a, const float* amp_perm, con
     PTG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, amp_perm, tw, pe, r));
 }
 
+template <int OP, bool PROBE>
+void launch_rmw2_t(Plan& p, const FrameArgs<float>& a, const float* amp_perm, const float2* tw, float2* grad,
+                   int kbeg, int kend) {
+    constexpr size_t smem = cl_smem_bytes<8, 32>();
+    auto kern = frame_rmw2_kernel<OP, PROBE>;
+    set_smem_attr(kern, smem);
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = p.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 8;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (!p.rmw_clusters) {
+        cfg.gridDim = dim3(8);
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, (void*)kern, &cfg) != cudaSuccess || ncl < 1) {
+            cudaGetLastError();
+            ncl = 148 / 8;
+        }
+        p.rmw_clusters = ncl;
+    }
+    const int ncl = std::max(1, std::min(p.rmw_clusters, kend - kbeg));
+    cfg.gridDim = dim3((unsigned)ncl * 8);
+    RmwArgs r{p.rmw_order.as<const int>(), p.rmw_dep_off.as<const int>(), p.rmw_dep_idx.as<const int>(),
+              p.rmw_done.as<unsigned>(), p.rmw_work.as<unsigned>(), grad, kbeg, kend};
+    const float2* pe = PROBE ? probe_epi_table(p, OP) : nullptr;
+    PTG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, amp_perm, tw, pe, r));
+}
+
 // frames [kbeg, kend) of the RMW order; the dispatch counter must be zero
 template <int OP>
 void launch_rmw(Plan& p, const FrameArgs<float>& a, const float* data, float2* grad, int kbeg, int kend) {
+    if (rmw2(p)) {
+        const float* ap = cl_amp(p, data, kSplitLine);
+        const float2* tw = cl_twiddles(p);
+        a.probe ? launch_rmw2_t<OP, true>(p, a, ap, tw, grad, kbeg, kend)
+                : launch_rmw2_t<OP, false>(p, a, ap, tw, grad, kbeg, kend);
+        return;
+    }
     const float* ap = cl_amp(p, data, rmw_line(p));
     const float2* tw = cl_twiddles(p);
     if (p.M == 128)
