@@ -283,11 +283,14 @@ int cl_line(const Plan& p) {
     return env == 64 ? 64 : 32;
 }
 constexpr int kSplitLine = 33;   // cl_amp tag: the split (two threads per line) order of frame_rmw2_kernel
-// M = 256 RMW plans use frame_rmw2_kernel (512 threads, two per line) unless PTG_RMW2=0
+// PTG_RMW2=1: M = 256 RMW plans use frame_rmw2_kernel (512 threads, two per
+// line: 46 % warps active instead of 23 %).  Measured and kept off by default:
+// 24.7 vs 22.1 ms per config-5 evaluation -- barrier (26 %) and MIO-throttle
+// (21 %) stalls grow with the extra shared-memory reads of the split lines
 bool rmw2(const Plan& p) {
     if (p.M != 256) return false;
     const char* e = getenv("PTG_RMW2");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
 }
 // local line of the persistent RMW kernel: 8-CTA (M = 256) / 4-CTA (M = 128)
 // clusters of 32-row CTAs.  Measured and rejected: 16-CTA clusters of 16-row

@@ -161,9 +161,11 @@ def test_config5_full_properties():
 
 
 # ------------------------------------------------ RMW overlap-add (frame_rmw.cuh)
-@pytest.mark.parametrize("M,steps,step,jitter,metric", [(128, 6, 40, 0, 0), (128, 7, 24, 2, 0), (256, 4, 48, 0, 0),
-                                                        (256, 5, 64, 3, 0), (256, 4, 48, 0, 1)])
-def test_rmw_matches_oracle(oracle, monkeypatch, M, steps, step, jitter, metric):
+@pytest.mark.parametrize("M,steps,step,jitter,metric,rmw2", [(128, 6, 40, 0, 0, 0), (128, 7, 24, 2, 0, 0),
+                                                             (256, 4, 48, 0, 0, 0), (256, 5, 64, 3, 0, 0),
+                                                             (256, 4, 48, 0, 1, 0), (256, 5, 48, 3, 0, 1),
+                                                             (256, 4, 48, 0, 1, 1)])
+def test_rmw_matches_oracle(oracle, monkeypatch, M, steps, step, jitter, metric, rmw2):
     """The persistent dependency-ordered RMW path (forced for small problems
     with PTG_NO_PLANES=1): odd window columns (jitter), both metrics, shift."""
     from paper_1810_05628_b200 import Plan, synth
@@ -177,6 +179,7 @@ def test_rmw_matches_oracle(oracle, monkeypatch, M, steps, step, jitter, metric)
     prob = oracle.Problem(n, M, M, pos, data.astype(np.float64), probe, metric)
     monkeypatch.setenv("PTG_NO_PLANES", "1")
     monkeypatch.setenv("PTG_RMW", "1")
+    monkeypatch.setenv("PTG_RMW2", str(rmw2))   # frame_rmw2_kernel (two threads per line)
     plan = Plan(n, M, M, pos, data, probe, precision="c64")
     for vv in (v, None):
         gv, gg = plan.evaluate(z, vv, metric=metric)
