@@ -1877,7 +1877,12 @@ static void eval_host_rmw(Plan& p, int metric, const double* z, double* value, d
         PTG_CUDA(cudaStreamCreateWithFlags(&p.s_in2, cudaStreamNonBlocking));
         PTG_CUDA(cudaStreamCreateWithFlags(&p.s_out2, cudaStreamNonBlocking));
     }
-    const cudaStream_t sin[2] = {p.s_in, p.s_in2}, sout[2] = {p.s_out, p.s_out2};
+    // one stream per direction by default: with two H2D streams both copy
+    // engines take the uploads queued up front and the downloads wait behind
+    // them (PTG_E2E_STREAMS=2 restores two per direction, A/B)
+    const char* es = getenv("PTG_E2E_STREAMS");
+    const bool two = es && atoi(es) == 2;
+    const cudaStream_t sin[2] = {p.s_in, two ? p.s_in2 : p.s_in}, sout[2] = {p.s_out, two ? p.s_out2 : p.s_out};
     while (p.ev_band.size() < (size_t)(2 * K + 4)) {
         cudaEvent_t e;
         PTG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
