@@ -1869,7 +1869,8 @@ static void eval_host_rmw(Plan& p, int metric, const double* z, double* value, d
     const int n = p.n, w = p.w, N = p.N;
     const size_t nn = p.nn();
     const char* eb = getenv("PTG_RMW_BANDS");
-    const int K = eb ? std::max(1, std::min(64, atoi(eb))) : 16;   // 16: 35.8 ms per config-5 call, 8: 36.6, 4: 39.9, unbanded 62.8
+    // config-5 ms per call (one copy stream per direction): 32 bands 26.4, 16: 26.8, 8: 28.6; unbanded 62.8
+    const int K = eb ? std::max(1, std::min(64, atoi(eb))) : 32;
     const int H = (n + K - 1) / K;
     if (!p.s_in) {
         PTG_CUDA(cudaStreamCreateWithFlags(&p.s_in, cudaStreamNonBlocking));
