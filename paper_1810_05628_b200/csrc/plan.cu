@@ -1035,37 +1035,64 @@ void build_rmw(Plan& p) {
     // gradient locality in L2), which costs more than the waits
     const char* esb = getenv("PTG_RMW_SB");
     const int gap = std::max(1, esb ? atoi(esb) : w / 8);
+    // row groups [s, e) of the row-sorted positions
+    std::vector<std::pair<int, int>> rows_g;
     for (int s = 0; s < N;) {
         int e = s + 1;
         while (e < N && r0(idx[e]) - r0(idx[s]) < gap) ++e;
+        rows_g.emplace_back(s, e);
+        s = e;
+    }
+    // PTG_RMW_PAIR=S (A/B): colour scan rows R and R + S together (rows S
+    // apart do not overlap when S w-steps >= w), doubling the frames per
+    // colour class while keeping the rows of a block of 2 S scan rows in L2
+    std::vector<std::vector<std::pair<int, int>>> groups;
+    const char* epair = getenv("PTG_RMW_PAIR");
+    const int S = epair ? atoi(epair) : 0;
+    if (S > 0) {
+        const int G0 = (int)rows_g.size();
+        for (int b = 0; b < G0; b += 2 * S)
+            for (int i = 0; i < S && b + i < G0; ++i) {
+                groups.push_back({rows_g[b + i]});
+                if (b + i + S < G0) groups.back().push_back(rows_g[b + i + S]);
+            }
+    } else {
+        for (auto& g : rows_g) groups.push_back({g});
+    }
+    for (const auto& grp : groups) {
+        std::vector<int> mem;   // positions into idx, ascending row
+        for (const auto& [s, e] : grp)
+            for (int i = s; i < e; ++i) mem.push_back(i);
         // greedy colouring of the group through a grid of w x w cells
-        std::vector<int> col(e - s, 0);
+        std::vector<int> col(mem.size(), 0);
         int ncol = 0;
         {
             const int Gc = std::max(1, (p.n + w - 1) / w);
-            const int rbase = r0(idx[s]) / w;
-            const int Gr = (r0(idx[e - 1]) / w) - rbase + 1;
-            std::vector<std::vector<int>> cell((size_t)Gr * Gc);
-            for (int i = s; i < e; ++i) {
+            const int rbase = r0(idx[mem.front()]) / w;
+            const int Gr = (r0(idx[mem.back()]) / w) - rbase + 1;
+            std::vector<std::vector<int>> cell((size_t)Gr * Gc);   // member slots
+            for (size_t a2 = 0; a2 < mem.size(); ++a2) {
+                const int i = mem[a2];
                 const int cy = r0(idx[i]) / w - rbase, cx = std::min(c0(idx[i]) / w, Gc - 1);
                 std::vector<char> used(ncol + 1, 0);
                 for (int yy = std::max(0, cy - 1); yy <= std::min(Gr - 1, cy + 1); ++yy)
                     for (int xx = std::max(0, cx - 1); xx <= std::min(Gc - 1, cx + 1); ++xx)
-                        for (int i2 : cell[(size_t)yy * Gc + xx])
-                            if (overlap(idx[i], idx[i2])) used[col[i2 - s]] = 1;
+                        for (int b2 : cell[(size_t)yy * Gc + xx])
+                            if (overlap(idx[i], idx[mem[b2]])) used[col[b2]] = 1;
                 int c = 0;
                 while (c < (int)used.size() && used[c]) ++c;
-                col[i - s] = c;
+                col[a2] = c;
                 ncol = std::max(ncol, c + 1);
-                cell[(size_t)cy * Gc + cx].push_back(i);
+                cell[(size_t)cy * Gc + cx].push_back((int)a2);
             }
         }
+        int maxr = 0;
         for (int c = 0; c < ncol; ++c)
-            for (int i = s; i < e; ++i)
-                if (col[i - s] == c) order.push_back(idx[i]);
+            for (size_t a2 = 0; a2 < mem.size(); ++a2)
+                if (col[a2] == c) order.push_back(idx[mem[a2]]);
+        for (int i : mem) maxr = std::max(maxr, r0(idx[i]));
         p.rmw_group_end.push_back((int)order.size());
-        p.rmw_group_maxr0.push_back(r0(idx[e - 1]));
-        s = e;
+        p.rmw_group_maxr0.push_back(maxr);
     }
     p.rmw_sufmin_r0.assign(N + 1, p.n);
     for (int k = N - 1; k >= 0; --k) p.rmw_sufmin_r0[k] = std::min(p.rmw_sufmin_r0[k + 1], r0(order[k]));
