@@ -1167,14 +1167,21 @@ void build_chunks(Plan& p) {
     // RMW overlap-add for the cluster path when the planes do not fit
     // (PTG_NO_RMW=1 selects the stash + gather path instead; read per plan)
     const bool no_rmw = getenv("PTG_NO_RMW") && getenv("PTG_NO_RMW")[0] == '1';
+    bool budget_override_off = false;
     // (the RMW order needs many more frames per colour class than clusters in
-    // flight: problems whose stash fits one chunk (configs 3-4) keep the
-    // stash + gather path; PTG_RMW=1 forces RMW)
-    const bool force_rmw = getenv("PTG_RMW") && getenv("PTG_RMW")[0] == '1';
+    // flight: M = 256 scans of >= 2000 positions (configs 4-5: config 4 3.15
+    // vs 3.06 ms on the device but 6.5 vs 12.9 ms end to end and a quarter of
+    // the DRAM traffic) or stashes that need several chunks; small scans keep
+    // stash + gather (config 3: 0.16 vs 1.06 ms).  PTG_RMW=1 / 0 forces.)
+    const char* erm = getenv("PTG_RMW");
+    const bool force_rmw = erm && erm[0] == '1';
+    if (erm && erm[0] == '0') budget_override_off = true;
     const size_t stash_bytes = (size_t)p.N * p.w * stash_pitch(p.w) * p.celem();
     size_t budget_b = (size_t)2 << 30;
     if (const char* e = getenv("PTG_STASH_BUDGET_MB")) budget_b = std::max<size_t>(1, (size_t)atoll(e)) << 20;
-    p.rmw_mode = (!p.planes_mode && p.cl && p.w == p.M && p.N > 0 && !no_rmw && (force_rmw || stash_bytes > budget_b)) ||
+    const bool big = stash_bytes > budget_b || (p.M == 256 && p.N >= 2000);
+    p.rmw_mode = (!p.planes_mode && p.cl && p.w == p.M && p.N > 0 && !no_rmw && !budget_override_off &&
+                  (force_rmw || big)) ||
                  (p.rows != p.n && p.N > 0);
     if (p.rmw_mode) {   // one chunk, no tile lists, no stash
         auto c = std::make_unique<Chunk>();
