@@ -1171,15 +1171,17 @@ void build_chunks(Plan& p) {
     // (the RMW order needs many more frames per colour class than clusters in
     // flight: M = 256 scans of >= 2000 positions (configs 4-5: config 4 3.15
     // vs 3.06 ms on the device but 6.5 vs 12.9 ms end to end and a quarter of
-    // the DRAM traffic) or stashes that need several chunks; small scans keep
-    // stash + gather (config 3: 0.16 vs 1.06 ms).  PTG_RMW=1 / 0 forces.)
+    // the DRAM traffic; config 5 22.3 vs 23.0 ms); small scans keep stash +
+    // gather (config 3: 0.16 vs 1.06 ms).  PTG_RMW=1 / 0 forces.)
     const char* erm = getenv("PTG_RMW");
     const bool force_rmw = erm && erm[0] == '1';
     if (erm && erm[0] == '0') budget_override_off = true;
     const size_t stash_bytes = (size_t)p.N * p.w * stash_pitch(p.w) * p.celem();
     size_t budget_b = (size_t)2 << 30;
     if (const char* e = getenv("PTG_STASH_BUDGET_MB")) budget_b = std::max<size_t>(1, (size_t)atoll(e)) << 20;
-    const bool big = stash_bytes > budget_b || (p.M == 256 && p.N >= 2000);
+    // (M = 128 keeps the stash even across chunks: config 5's level 1,
+    // 27,556 x 128^2, 4.38 ms stash vs 5.04 ms RMW)
+    const bool big = p.M == 256 && (stash_bytes > budget_b || p.N >= 2000);
     p.rmw_mode = (!p.planes_mode && p.cl && p.w == p.M && p.N > 0 && !no_rmw && !budget_override_off &&
                   (force_rmw || big)) ||
                  (p.rows != p.n && p.N > 0);
