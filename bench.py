@@ -243,6 +243,23 @@ def cpu_eval_rate(cfg, obj, probe, seconds: float, min_evals: int = 3):
             "ms_per_eval": med * 1e3, "patterns": p.N}
 
 
+def cpu_one_thread_rate(cfg, obj, probe):
+    """The same CPU sample on ONE thread (nproc and 1 thread)."""
+    from oracle import ptgo
+    kind = cpu_reference_on()
+    ptgo.set_threads(1)
+    try:
+        p, n, desc = cpu_problem(cfg, obj, probe)
+        z = np.ones((n, n), np.complex128)
+        t0 = time.perf_counter()
+        ptgo.evaluate(p, z)
+        dt = time.perf_counter() - t0
+    finally:
+        ptgo.set_threads(NPROC)
+    return {"value": p.N / dt, "unit": UNIT, "cores": 1, "kind": kind, "ms_per_eval": dt * 1e3,
+            "sample": f"1 objective+gradient eval of {p.N} patterns on one thread, {desc}"}
+
+
 def cpu_pie_sweep_ms(cfg, obj, probe):
     """PIE (solvers.cpp:229-265) on the host, ms per sweep: (t(3 sweeps) -
     t(1 sweep)) / 2 minus one evaluation (the uncounted diagnostic
@@ -665,6 +682,7 @@ def run_ours(args):
         # CPU baseline on a bounded sample of the same workload
         try:
             cpu = cpu_eval_rate(cfg, obj, probe, args.cpu_seconds)
+            cpu["one_thread"] = cpu_one_thread_rate(cfg, obj, probe)
         except Exception as ex:   # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": NPROC, "kind": "reference", "sample": f"failed: {ex}"}
         # the other BASELINE configurations, each beside its CPU reference rate

@@ -50,7 +50,13 @@ void ptgo_set_fft_hook(void *fn) { g_fft_hook = (ptgo_fft_fn)fn; }
 static int g_threads = 1;
 /* Pattern-parallel evaluation (results stay bitwise identical: per-pattern
  * contributions are accumulated in scan order afterwards). */
-void ptgo_set_threads(int t) { g_threads = t < 1 ? 1 : t; }
+void ptgo_set_threads(int t) {
+    g_threads = t < 1 ? 1 : t;
+    /* also the OpenMP default of the calling thread: the reference's
+       kernels::fft2_inplace parallelises its rows (kernels.cpp:126) whenever
+       it runs outside the position-parallel region -- t = 1 is one thread */
+    omp_set_num_threads(g_threads);
+}
 
 static int is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
