@@ -68,6 +68,10 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
     return make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 
+#ifndef PTG_RMW_BULK
+#define PTG_RMW_BULK 0
+#endif
+
 #ifdef ABL_TIMELINE   // diagnostic build: per-frame phase stamps of the first 64 CTAs (tools/rmw_timeline.py)
 constexpr int kRtlCtas = 64, kRtlFrames = 128, kRtlStamps = 12;
 __device__ unsigned long long g_rmw_tl[kRtlCtas * kRtlFrames * kRtlStamps];
@@ -366,6 +370,23 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         // (C) read-modify-write of this CTA's L object rows, coalesced; every
         //     load in flight at once (x[] is free again)
         float2* G0 = r.grad + (size_t)pj.x * n + pj.y;
+#if PTG_RMW_BULK
+        if ((pj.y & 1) == 0) {
+            // experiment (PTG_RMW_BULK=1): the update as TMA bulk reduce-adds,
+            // one 2 KiB object row per copy, smem contributions -> L2
+            if (t < L) {
+                fence_proxy_async_smem();
+                const int row = t, orow = q * NPC + row / Q + L * (row % Q);
+                asm volatile(
+                    "cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
+                        G0 + (size_t)orow * n),
+                    "r"(smem_u32(buf + row * PM)), "r"((uint32_t)(M * sizeof(float2)))
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            }
+        } else
+#endif
         if ((pj.y & 1) == 0) {
             constexpr int HW = M / 2, PER = L * HW / NT, HALF = PER / 2;   // float4 (pixel pairs) per thread
 #pragma unroll

@@ -461,12 +461,16 @@ void launch_rmw(Plan& p, const FrameArgs<float>& a, const float* data, float2* g
     }
     const float* ap = cl_amp(p, data, rmw_line(p));
     const float2* tw = cl_twiddles(p);
+    // PTG_ABL_NOPROBE=1: timing ablation only (the probe-free kernel on a
+    // probe problem: wrong results), measures what the probe loads cost
+    static const bool abl_noprobe = getenv("PTG_ABL_NOPROBE") && getenv("PTG_ABL_NOPROBE")[0] == '1';
+    const bool probe = a.probe && !abl_noprobe;
     if (p.M == 128)
-        a.probe ? launch_rmw_t<4, 32, OP, true>(p, a, ap, tw, grad, kbeg, kend)
-                : launch_rmw_t<4, 32, OP, false>(p, a, ap, tw, grad, kbeg, kend);
+        probe ? launch_rmw_t<4, 32, OP, true>(p, a, ap, tw, grad, kbeg, kend)
+              : launch_rmw_t<4, 32, OP, false>(p, a, ap, tw, grad, kbeg, kend);
     else
-        a.probe ? launch_rmw_t<8, 32, OP, true>(p, a, ap, tw, grad, kbeg, kend)
-                : launch_rmw_t<8, 32, OP, false>(p, a, ap, tw, grad, kbeg, kend);
+        probe ? launch_rmw_t<8, 32, OP, true>(p, a, ap, tw, grad, kbeg, kend)
+              : launch_rmw_t<8, 32, OP, false>(p, a, ap, tw, grad, kbeg, kend);
 }
 
 // objective frame kernel: TMA/register path for complex64 patch frames up to
