@@ -15,8 +15,10 @@
 //     consecutive window rows, inside a group greedy colour classes of
 //     pairwise non-overlapping windows, class by class.  That order is the
 //     summation order of every pixel -- fixed by the geometry, so results are
-//     bitwise reproducible run to run (no float atomics: every update is a
-//     plain load + add + store by the one frame that owns the pixel then);
+//     bitwise reproducible run to run (no unordered float atomics: a pixel
+//     is updated by one frame at a time -- a TMA bulk reduce-add of the
+//     frame's object row, or a plain load + add + store for windows that
+//     start on an odd column);
 //   * frame k may update the gradient only after every EARLIER overlapping
 //     frame has finished its update: a per-frame completion counter (one
 //     release-increment per CTA, CUTLASS GenericBarrier style) that the
@@ -68,9 +70,79 @@ __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
     return make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 
+// PTG_RMW_BULK: the gradient update of 16-byte-aligned windows as TMA bulk
+// reduce-adds (cp.reduce.async.bulk .add.f32, one 2 KiB object row per copy,
+// shared memory -> L2): the gradient rows are not read into the SM at all.
+// Still one add per pixel per frame, in the dependency order, so every pixel's
+// summation order is fixed.  Config 5 (ms per evaluation): 0 = load + add +
+// store 22.33; 1 = bulk, completion awaited before the publish 21.64
+// (default); 2 = completion awaited a gather later 22.14.
 #ifndef PTG_RMW_BULK
-#define PTG_RMW_BULK 0
+#define PTG_RMW_BULK 1
 #endif
+// PTG_RMW_PUSHBAR=1: the inverse pushes as st.async completing transaction
+// bytes on the owner's mbarrier (like the gather), so the owner waits for its
+// own 64 KiB instead of a third cluster-wide barrier per frame
+#ifndef PTG_RMW_PUSHBAR
+#define PTG_RMW_PUSHBAR 0
+#endif
+
+// TM = true (M = 256 probe frames, PTG_RMW_TMEM=0 turns it off at run time):
+// the probe rows of this CTA (the same 32 rows every frame, 32 values per
+// thread) are kept in tensor memory -- otherwise idle on this path -- and read
+// back with tcgen05.ld for the gather's probe multiply and the conj(P)
+// epilogue, instead of two 512 KiB L2 reads per frame.  TMEM is used purely as
+// thread-private storage (32x32b: lane = thread, 64 columns per warp, 128
+// columns per CTA, two CTAs per SM), no MMA.  conj(sc P) is formed from P on
+// the fly (sc a power of two: exact, the probe_epi table's bits).  Config 5:
+// 21.66 -> 20.61 ms per evaluation.  cudaOccupancyMaxActiveClusters reports
+// 15 instead of 33 clusters for a kernel that allocates tensor memory, so the
+// grid is sized with the TM = false instantiation (same registers and shared
+// memory); 33 clusters are co-resident (tools/tmem_probe.cu: two CTAs of one
+// SM hold their allocations at once), and the dispatch protocol does not
+// depend on co-residency anyway.
+
+// 2 W 32-bit TMEM columns <-> W float2 registers of this thread (W = 4 | 8);
+// the load includes its wait so the outputs are valid after the statement
+template <int W>
+__device__ __forceinline__ void tmem_st_f2(uint32_t taddr, const float2* v) {
+    static_assert(W == 4 || W == 8, "tmem_st_f2: 4 or 8 values");
+    if constexpr (W == 8) {
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15, %16};" ::"r"(taddr),
+            "f"(v[0].x), "f"(v[0].y), "f"(v[1].x), "f"(v[1].y), "f"(v[2].x), "f"(v[2].y), "f"(v[3].x), "f"(v[3].y),
+            "f"(v[4].x), "f"(v[4].y), "f"(v[5].x), "f"(v[5].y), "f"(v[6].x), "f"(v[6].y), "f"(v[7].x), "f"(v[7].y)
+            : "memory");
+    } else {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                     "f"(v[0].x), "f"(v[0].y), "f"(v[1].x), "f"(v[1].y), "f"(v[2].x), "f"(v[2].y), "f"(v[3].x),
+                     "f"(v[3].y)
+                     : "memory");
+    }
+}
+template <int W>
+__device__ __forceinline__ void tmem_ld_f2(uint32_t taddr, float2* v) {
+    static_assert(W == 4 || W == 8, "tmem_ld_f2: 4 or 8 values");
+    if constexpr (W == 8) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15}, [%16];\n\ttcgen05.wait::ld.sync.aligned;"
+            : "=f"(v[0].x), "=f"(v[0].y), "=f"(v[1].x), "=f"(v[1].y), "=f"(v[2].x), "=f"(v[2].y), "=f"(v[3].x),
+              "=f"(v[3].y), "=f"(v[4].x), "=f"(v[4].y), "=f"(v[5].x), "=f"(v[5].y), "=f"(v[6].x), "=f"(v[6].y),
+              "=f"(v[7].x), "=f"(v[7].y)
+            : "r"(taddr)
+            : "memory");
+    } else {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t"
+            "tcgen05.wait::ld.sync.aligned;"
+            : "=f"(v[0].x), "=f"(v[0].y), "=f"(v[1].x), "=f"(v[1].y), "=f"(v[2].x), "=f"(v[2].y), "=f"(v[3].x),
+              "=f"(v[3].y)
+            : "r"(taddr)
+            : "memory");
+    }
+}
 
 #ifdef ABL_TIMELINE   // diagnostic build: per-frame phase stamps of the first 64 CTAs (tools/rmw_timeline.py)
 constexpr int kRtlCtas = 64, kRtlFrames = 128, kRtlStamps = 12;
@@ -87,7 +159,7 @@ __device__ unsigned long long g_rmw_tl[kRtlCtas * kRtlFrames * kRtlStamps];
 #define RTL(k)
 #endif
 
-template <int Q, int L, int OP, bool PROBE>
+template <int Q, int L, int OP, bool PROBE, bool TM = false>
 __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
     frame_rmw_kernel(FrameArgs<float> a, const float* __restrict__ amp_perm, const float2* __restrict__ tw_g,
                      const float2* __restrict__ probe_epi, RmwArgs r) {
@@ -101,6 +173,9 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
     float* amp_s = reinterpret_cast<float*>(tw + M);     // [L][AP]
     __shared__ double red[NT / 32];
     __shared__ __align__(8) unsigned long long bar_a, bar_g;
+#if PTG_RMW_PUSHBAR
+    __shared__ __align__(8) unsigned long long bar_p;
+#endif
     __shared__ int4 s_item;   // (order index k, position j, window row, window column) of this frame
 
     const int q = (int)cl.block_rank();
@@ -109,9 +184,38 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
     if (t == 0) {
         mbar_init(&bar_g, 1);
         mbar_init(&bar_a, 1);
+#if PTG_RMW_PUSHBAR
+        mbar_init(&bar_p, 1);
+#endif
         fence_mbarrier_init();
     }
     for (int i = t; i < M; i += NT) tw[i] = __ldg(tw_g + i);
+    // probe rows q NPC + b + L s, column t -> this thread's TMEM lane, columns
+    // 2 Q b .. 2 Q b + 2 Q - 1 of its warp's 64-column block
+    static_assert(!TM || (PROBE && NT <= 256), "tensor-memory probe cache: probe frames, <= 8 warps");
+    __shared__ uint32_t s_tmem;
+    uint32_t tm = 0;
+    if constexpr (TM) {
+        if (t < 32) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                         "r"(128u)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int wp = t >> 5;
+        tm = s_tmem + ((uint32_t)((wp & 3) * 32) << 16) + (uint32_t)((wp >> 2) * 64);
+#pragma unroll
+        for (int b = 0; b < NPC; ++b) {
+            float2 pv[Q];
+#pragma unroll
+            for (int s = 0; s < Q; ++s) pv[s] = __ldg(a.probe + (size_t)(q * NPC + b + L * s) * M + t);
+            tmem_st_f2<Q>(tm + 2 * Q * b, pv);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
     // Rank 0 (thread 0) claims the next frame one frame ahead and fetches its
     // position index and window: three dependent L2 round trips, spread over
     // the current frame's phases (claim at the loop top, index after the
@@ -133,6 +237,17 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
     const int rr = t % L, qq = t / L;
     const uint32_t bar_g_u = smem_u32(&bar_g), buf_u = smem_u32(buf);
     uint32_t ph = 0;
+#if PTG_RMW_BULK == 2
+    int pend_k = -1;   // warp 0: frame whose bulk reduce-adds are in flight (published once they complete)
+    auto publish_pending = [&]() {
+        if (t < 32 && pend_k >= 0) {
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            __syncwarp();
+            if (t == 0) red_release_gpu_add(r.done + pend_k, 1u);
+            pend_k = -1;
+        }
+    };
+#endif
 
 #ifdef ABL_TIMELINE
     int rtl_f = 0;
@@ -144,6 +259,9 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         // cluster; the full cluster barrier also orders every CTA's previous
         // epilogue (reads of its own rows) before the pushes of this frame
         if (t == 0) mbar_arrive_expect_tx(&bar_g, (uint32_t)(L * M * sizeof(float2)));
+#if PTG_RMW_PUSHBAR
+        if (t == 0) mbar_arrive_expect_tx(&bar_p, (uint32_t)(L * M * sizeof(float2)));
+#endif
         if (q == 0 && t == 0) {
 #pragma unroll
             for (int s = 0; s < Q; ++s) {
@@ -178,7 +296,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         float2 x[L];
         {
             const float2* zc = a.z + (size_t)pj.x * n + pj.y + t;
-            float2 zb[2][Q], pb[2][Q];
+            float2 zb[2][Q], pb[TM ? 1 : 2][Q];   // TM: probe values read from tensor memory at use
             const size_t zstep = (size_t)L * n;
             auto load = [&](int b, int u) {
                 // rows q NPC + b + L s through running pointers (one live
@@ -190,7 +308,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                 for (int s = 0; s < Q; ++s) {
                     zb[u][s] = ldg_pinned(zp);
                     zp += zstep;
-                    if constexpr (PROBE) {
+                    if constexpr (PROBE && !TM) {
                         pb[u][s] = ldg_pinned(pp);
                         pp += (size_t)L * M;
                     }
@@ -203,8 +321,9 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                 const int u = b & 1;
                 const int rw = q * NPC + b;
                 float2 v[Q];
+                if constexpr (TM) tmem_ld_f2<Q>(tm + 2 * Q * b, pb[0]);
 #pragma unroll
-                for (int s = 0; s < Q; ++s) v[s] = PROBE ? cmul(pb[u][s], zb[u][s]) : zb[u][s];
+                for (int s = 0; s < Q; ++s) v[s] = PROBE ? cmul(pb[TM ? 0 : u][s], zb[u][s]) : zb[u][s];
                 if (b + 2 < NPC) load(b + 2, u);
                 dft_q<Q>(v);
 #pragma unroll
@@ -216,6 +335,9 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         }
         if (leader && next.x < r.kend) next.y = __ldg(r.order + next.x);
         RTL(2);
+#if PTG_RMW_BULK == 2
+        publish_pending();   // the previous frame's reduce-adds landed during this gather
+#endif
         mbar_wait(&bar_g, ph);   // all Q senders' rows have landed in this CTA
         RTL(3);
 
@@ -312,14 +434,32 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                 RTL(6);
             } else {
                 asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+#if PTG_RMW_PUSHBAR
+                const uint32_t bar_p_u = smem_u32(&bar_p);
+#pragma unroll
+                for (int kk = 0; kk < L; ++kk)   // remote row (kk % NPC) Q + q of CTA kk / NPC
+                    st_async_f2(mapa_u32(buf_u + (uint32_t)((((kk % NPC) * Q + q) * PM + t) * sizeof(float2)),
+                                         kk / NPC),
+                                x[kk], mapa_u32(bar_p_u, kk / NPC));
+#else
 #pragma unroll
                 for (int kk = 0; kk < L; ++kk)   // remote row (kk % NPC) Q + q of CTA kk / NPC
                     st_cluster_f2(mapa_u32(buf_u + (uint32_t)((((kk % NPC) * Q + q) * PM + t) * sizeof(float2)),
                                            kk / NPC),
                                   x[kk]);
+#endif
             }
         }
-        if constexpr (PROBE) {
+        if constexpr (TM) {
+            const float scp = (OP == OP_DISTANCE) ? 1.f / (float(M) * float(M)) : 2.f;
+#pragma unroll
+            for (int i = 0; i < NPC; ++i) {
+                float2 pv[Q];
+                tmem_ld_f2<Q>(tm + 2 * Q * i, pv);
+#pragma unroll
+                for (int s = 0; s < Q; ++s) x[i * Q + s] = make_float2(pv[s].x * scp, -(pv[s].y * scp));
+            }
+        } else if constexpr (PROBE) {
 #pragma unroll
             for (int i = 0; i < NPC; ++i)
 #pragma unroll
@@ -329,7 +469,12 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if ((t & 31) == 0) red[t / 32] = acc;
         RTL(7);
+#if PTG_RMW_PUSHBAR
+        mbar_wait(&bar_p, ph);   // this CTA's rows have landed (all Q senders)
+        __syncthreads();         // red[] of every warp
+#else
         cl.sync();   // every push has landed; no remote access to this CTA's rows until the next frame
+#endif
         RTL(8);
         if (t == 0) {
             double s = 0.0;
@@ -372,8 +517,8 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         float2* G0 = r.grad + (size_t)pj.x * n + pj.y;
 #if PTG_RMW_BULK
         if ((pj.y & 1) == 0) {
-            // experiment (PTG_RMW_BULK=1): the update as TMA bulk reduce-adds,
-            // one 2 KiB object row per copy, smem contributions -> L2
+            // the update as TMA bulk reduce-adds, one 2 KiB object row per
+            // copy, smem contributions -> L2
             if (t < L) {
                 fence_proxy_async_smem();
                 const int row = t, orow = q * NPC + row / Q + L * (row % Q);
@@ -383,7 +528,14 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                     "r"(smem_u32(buf + row * PM)), "r"((uint32_t)(M * sizeof(float2)))
                     : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+#if PTG_RMW_BULK == 2
+                // only the shared-memory source must be free before the next
+                // frame's pushes; completion is awaited a gather later
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                pend_k = k;
+#else
                 asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#endif
             }
         } else
 #endif
@@ -426,13 +578,29 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
             }
         }
         // (D) publish: this CTA's rows of frame k are final
+#if PTG_RMW_BULK == 2
+        if ((pj.y & 1) != 0) {   // (uniform) plain-store frames publish now; bulk frames once their adds complete
+            __syncthreads();
+            if (t == 0) red_release_gpu_add(r.done + k, 1u);
+        }
+#else
         __syncthreads();
         if (t == 0) red_release_gpu_add(r.done + k, 1u);
+#endif
         RTL(11);
 #ifdef ABL_TIMELINE
         ++rtl_f;
 #endif
         ph ^= 1u;
+    }
+#if PTG_RMW_BULK == 2
+    publish_pending();
+#endif
+    if constexpr (TM) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (t < 32)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(128u) : "memory");
     }
 }
 

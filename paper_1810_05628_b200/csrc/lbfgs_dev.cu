@@ -414,20 +414,44 @@ __global__ void __launch_bounds__(kReduceThreads) k_multi_dot(const MultiDotArgs
     double acc[kMdPairs * 4];
 #pragma unroll
     for (int k = 0; k < kMdPairs * 4; ++k) acc[k] = 0.0;
+    // Every load of an element is issued before any product (one HBM round
+    // trip per element instead of one per pair: the history is 2 x 25 vectors,
+    // far beyond L2 at the larger levels).  Rows past A read pair A - 1 again
+    // (never stored); the fresh pair reads zn / gn in place of its own s / y,
+    // which k_pair_stats may be writing concurrently.  Same products, same
+    // order of additions as the pair-by-pair loop: same bits.
+    const bool any_fresh = a.zn && p0 + kMdPairs >= a.A && p0 < a.A;
+    const C* sp[kMdPairs];
+    const C* yp[kMdPairs];
+    bool fr[kMdPairs];
+#pragma unroll
+    for (int q = 0; q < kMdPairs; ++q) {
+        const int pq = min(p0 + q, a.A - 1);
+        fr[q] = a.zn && pq == a.A - 1;
+        sp[q] = fr[q] ? a.zn : a.s[pq];
+        yp[q] = fr[q] ? a.gn : a.y[pq];
+    }
+    const C* zop = any_fresh ? a.zo : a.gn;
+#pragma unroll 2
     for (size_t i = lo + threadIdx.x; i < hi; i += kReduceThreads) {
         const C gn = a.gn[i];
-        const C yc = a.zn ? csub(gn, a.go[i]) : a.yc[i];
+        const C yo = a.zn ? a.go[i] : a.yc[i];
+        const C zo = zop[i];
+        C svr[kMdPairs], yvr[kMdPairs];
 #pragma unroll
         for (int q = 0; q < kMdPairs; ++q) {
-            if (p0 + q < a.A) {
-                const bool fresh = a.zn && p0 + q == a.A - 1;
-                const C sv = fresh ? csub(a.zn[i], a.zo[i]) : a.s[p0 + q][i];
-                const C yv = fresh ? yc : a.y[p0 + q][i];
-                acc[4 * q + 0] = __dadd_rn(acc[4 * q + 0], dot_term(sv, yc));
-                acc[4 * q + 1] = __dadd_rn(acc[4 * q + 1], dot_term(yv, yc));
-                acc[4 * q + 2] = __dadd_rn(acc[4 * q + 2], dot_term(sv, gn));
-                acc[4 * q + 3] = __dadd_rn(acc[4 * q + 3], dot_term(yv, gn));
-            }
+            svr[q] = sp[q][i];
+            yvr[q] = yp[q][i];
+        }
+        const C yc = a.zn ? csub(gn, yo) : yo;
+#pragma unroll
+        for (int q = 0; q < kMdPairs; ++q) {
+            const C sv = fr[q] ? csub(svr[q], zo) : svr[q];
+            const C yv = fr[q] ? yc : yvr[q];
+            acc[4 * q + 0] = __dadd_rn(acc[4 * q + 0], dot_term(sv, yc));
+            acc[4 * q + 1] = __dadd_rn(acc[4 * q + 1], dot_term(yv, yc));
+            acc[4 * q + 2] = __dadd_rn(acc[4 * q + 2], dot_term(sv, gn));
+            acc[4 * q + 3] = __dadd_rn(acc[4 * q + 3], dot_term(yv, gn));
         }
     }
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;

@@ -384,8 +384,17 @@ void launch_cl(Plan& p, const FrameArgs<float>& a, int count, const float* data)
 template <int Q, int L, int OP, bool PROBE>
 void launch_rmw_t(Plan& p, const FrameArgs<float>& a, const float* amp_perm, const float2* tw, float2* grad,
                   int kbeg, int kend) {
-    constexpr size_t smem = cl_smem_bytes<Q, L>();
-    auto kern = frame_rmw_kernel<Q, L, OP, PROBE>;
+    // PTG_RMW_SMEM_PAD=bytes (diagnostic): extra dynamic shared memory, e.g. to
+    // force one CTA per SM and read off how much two co-resident frames overlap
+    static const size_t pad = getenv("PTG_RMW_SMEM_PAD") ? (size_t)atoll(getenv("PTG_RMW_SMEM_PAD")) : 0;
+    const size_t smem = cl_smem_bytes<Q, L>() + pad;
+    // probe rows cached in tensor memory (frame_rmw.cuh): M = 256 probe frames
+    constexpr bool TMC = PROBE && Q == 8;
+    static const bool tm_off = getenv("PTG_RMW_TMEM") && getenv("PTG_RMW_TMEM")[0] == '0';   // A/B switch
+    const bool tm = TMC && !tm_off;
+    auto kern_sizing = frame_rmw_kernel<Q, L, OP, PROBE, false>;   // occupancy query (see frame_rmw.cuh)
+    auto kern = tm ? frame_rmw_kernel<Q, L, OP, PROBE, TMC> : kern_sizing;
+    set_smem_attr(kern_sizing, smem);
     set_smem_attr(kern, smem);
     cudaLaunchConfig_t cfg{};
     cfg.blockDim = dim3(Q * L);
@@ -401,10 +410,13 @@ void launch_rmw_t(Plan& p, const FrameArgs<float>& a, const float* amp_perm, con
     if (!p.rmw_clusters) {   // persistent grid: the clusters that fit at once
         cfg.gridDim = dim3(Q);
         int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, (void*)kern, &cfg) != cudaSuccess || ncl < 1) {
+        if (cudaOccupancyMaxActiveClusters(&ncl, (void*)kern_sizing, &cfg) != cudaSuccess || ncl < 1) {
             cudaGetLastError();
             ncl = 148 / Q;
         }
+        // PTG_RMW_CLUSTERS=C (diagnostic): override the persistent grid
+        if (const char* e = getenv("PTG_RMW_CLUSTERS")) ncl = std::max(1, atoi(e));
+        if (getenv("PTG_RMW_DEBUG")) fprintf(stderr, "[rmw] Q=%d L=%d: %d co-resident clusters, %zu B smem/CTA\n", Q, L, ncl, smem);
         p.rmw_clusters = ncl;
     }
     const int ncl = std::max(1, std::min(p.rmw_clusters, kend - kbeg));

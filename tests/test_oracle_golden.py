@@ -96,3 +96,23 @@ def test_mgopt_bitwise(oracle, gold, depth):
     meta = gold[f"mg{depth}_meta"]
     assert [r.value, r.weighted, r.reason] == list(meta[:3])
     assert r.per_level == [int(x) for x in meta[3:]]
+
+
+MG_DEFAULT = os.path.join(os.path.dirname(__file__), "golden", "mg_default_golden.npz")
+
+
+@pytest.mark.parametrize("tag", ["a", "b"])
+def test_mgopt_default_settings_bitwise(oracle, tag):
+    """Depth-3 MG/OPT at the reference's default settings (coarsest solve 100
+    LBFGS iterations, multigrid.cpp:123-128) on data with the reference's
+    addNoise: golden run by the unmodified reference (make_mg_default_golden.py)."""
+    gold = dict(np.load(MG_DEFAULT))
+    n, w, s, depth = (int(v) for v in gold[f"{tag}_geom"])
+    h = oracle.Hierarchy(oracle.Problem(n, n, w, gold[f"{tag}_pos"], gold[f"{tag}_data"]), depth)
+    assert h.coarsest_iters() == 100
+    r = h.driver(gold[f"{tag}_z0"], budget=1e9, max_cycles=3)
+    meta = gold[f"{tag}_meta"]
+    assert np.array_equal(r.z, gold[f"{tag}_z"])
+    assert np.array_equal(r.history, gold[f"{tag}_hist"])
+    assert [r.value, r.weighted, r.reason] == list(meta[:3])
+    assert r.per_level == [int(x) for x in meta[3:]]
