@@ -448,6 +448,9 @@ def roofline_for(cfg, N, frame_ms, frame_n, steps):
     traffic = prof.get("dram_bytes_per_launch") if isinstance(prof, dict) else prof
     if cfg.M <= 64 and cfg.precision == "c64":
         kname = f"frame_tma_kernel<{cfg.M}> (TMA-fed register FFT, one CTA per scan position)"
+    elif cfg.precision == "c64" and cfg.M == 256 and N >= 2000:
+        kname = ("frame_rmw_kernel<8,32> (persistent clusters of 8 CTAs, one scan position per cluster at a time, "
+                 "dependency-ordered in-place overlap-add, probe rows + next object window in tensor memory)")
     elif cfg.precision == "c64":
         kname = f"frame_cl_kernel<{cfg.M // 32},32> (cluster of {cfg.M // 32} CTAs per scan position)"
     else:

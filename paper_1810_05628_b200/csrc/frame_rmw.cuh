@@ -144,6 +144,33 @@ __device__ __forceinline__ void tmem_ld_f2(uint32_t taddr, float2* v) {
     }
 }
 
+// two blocks in one statement, one wait (W = 8)
+__device__ __forceinline__ void tmem_ld2_f2(uint32_t ta, float2* va, uint32_t tb, float2* vb) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%32];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, "
+        "%29, %30, %31}, [%33];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=f"(va[0].x), "=f"(va[0].y), "=f"(va[1].x), "=f"(va[1].y), "=f"(va[2].x), "=f"(va[2].y), "=f"(va[3].x),
+          "=f"(va[3].y), "=f"(va[4].x), "=f"(va[4].y), "=f"(va[5].x), "=f"(va[5].y), "=f"(va[6].x), "=f"(va[6].y),
+          "=f"(va[7].x), "=f"(va[7].y), "=f"(vb[0].x), "=f"(vb[0].y), "=f"(vb[1].x), "=f"(vb[1].y), "=f"(vb[2].x),
+          "=f"(vb[2].y), "=f"(vb[3].x), "=f"(vb[3].y), "=f"(vb[4].x), "=f"(vb[4].y), "=f"(vb[5].x), "=f"(vb[5].y),
+          "=f"(vb[6].x), "=f"(vb[6].y), "=f"(vb[7].x), "=f"(vb[7].y)
+        : "r"(ta), "r"(tb)
+        : "memory");
+}
+
+// PTG_RMW_ZPREF (with TM, Q = 8): the NEXT frame's object window is fetched
+// during this frame's gradient update (registers are free there, the loads
+// overlap the dependency wait and the bulk reduce-adds) and parked in a second
+// tensor-memory block, so the gather of a frame is tensor-memory reads only:
+// no L2 round trip sits on the frame's critical path.  The item of frame k + 1
+// is handed to the cluster during frame k (before the inverse pushes' barrier).
+#ifndef PTG_RMW_ZPREF
+#define PTG_RMW_ZPREF 1
+#endif
+
 #ifdef ABL_TIMELINE   // diagnostic build: per-frame phase stamps of the first 64 CTAs (tools/rmw_timeline.py)
 constexpr int kRtlCtas = 64, kRtlFrames = 128, kRtlStamps = 12;
 __device__ unsigned long long g_rmw_tl[kRtlCtas * kRtlFrames * kRtlStamps];
@@ -176,7 +203,11 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
 #if PTG_RMW_PUSHBAR
     __shared__ __align__(8) unsigned long long bar_p;
 #endif
-    __shared__ int4 s_item;   // (order index k, position j, window row, window column) of this frame
+    // (order index k, position j, window row, window column) of a frame; ZP:
+    // [ph] this frame, [ph ^ 1] the next one (written during this frame)
+    __shared__ int4 s_item[2];
+    constexpr bool ZP = TM && Q == 8 && PTG_RMW_ZPREF != 0;
+    constexpr unsigned TCOLS = ZP ? 256u : 128u;
 
     const int q = (int)cl.block_rank();
     const int t = threadIdx.x;
@@ -198,7 +229,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
     if constexpr (TM) {
         if (t < 32) {
             asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
-                         "r"(128u)
+                         "r"(TCOLS)
                          : "memory");
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
         }
@@ -237,6 +268,53 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
     const int rr = t % L, qq = t / L;
     const uint32_t bar_g_u = smem_u32(&bar_g), buf_u = smem_u32(buf);
     uint32_t ph = 0;
+    // item `next` -> slot `slot` of every CTA of the cluster (leader thread)
+    auto hand_item = [&](int slot) {
+#pragma unroll
+        for (int s = 0; s < Q; ++s) {
+            const uint32_t base = mapa_u32(smem_u32(&s_item[slot]), s);
+            st_cluster_u32(base, (unsigned)next.x);
+            st_cluster_u32(base + 4, (unsigned)next.y);
+            st_cluster_u32(base + 8, (unsigned)next.z);
+            st_cluster_u32(base + 12, (unsigned)next.w);
+        }
+    };
+    // ZP: window (wr, wc) rows q NPC + b + L s, column t -> registers zv[b Q + s]
+    // (pinned loads: issued here, consumed by zpref_store)
+    const uint32_t tmz = tm + 128u;
+    auto zpref_issue = [&](int wr, int wc, float2* zv) {
+        const float2* zc = a.z + (size_t)wr * n + wc + t;
+        const size_t zstep = (size_t)L * n;
+#pragma unroll
+        for (int b = 0; b < NPC; ++b) {
+            const float2* zp = zc + (size_t)(q * NPC + b) * n;
+#pragma unroll
+            for (int s = 0; s < Q; ++s) {
+                zv[b * Q + s] = ldg_pinned(zp);
+                zp += zstep;
+            }
+        }
+    };
+    auto zpref_store = [&](const float2* zv) {
+#pragma unroll
+        for (int b = 0; b < NPC; ++b) tmem_st_f2<Q>(tmz + 2 * Q * b, zv + b * Q);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    };
+    if constexpr (ZP) {
+        // the first item to every CTA, its window into tensor memory
+        if (leader) {
+            hand_item(0);
+            next.x = r.kbeg + (int)atomicAdd(r.work, 1u);
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        const int4 it0 = s_item[0];
+        if (it0.x < r.kend) {
+            float2 zv[L];
+            zpref_issue(it0.z, it0.w, zv);
+            zpref_store(zv);
+        }
+    }
 #if PTG_RMW_BULK == 2
     int pend_k = -1;   // warp 0: frame whose bulk reduce-adds are in flight (published once they complete)
     auto publish_pending = [&]() {
@@ -262,20 +340,15 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
 #if PTG_RMW_PUSHBAR
         if (t == 0) mbar_arrive_expect_tx(&bar_p, (uint32_t)(L * M * sizeof(float2)));
 #endif
-        if (q == 0 && t == 0) {
-#pragma unroll
-            for (int s = 0; s < Q; ++s) {
-                const uint32_t base = mapa_u32(smem_u32(&s_item), s);
-                st_cluster_u32(base, (unsigned)next.x);
-                st_cluster_u32(base + 4, (unsigned)next.y);
-                st_cluster_u32(base + 8, (unsigned)next.z);
-                st_cluster_u32(base + 12, (unsigned)next.w);
+        if constexpr (!ZP) {
+            if (leader) {
+                hand_item(0);
+                next.x = r.kbeg + (int)atomicAdd(r.work, 1u);   // the following frame, claimed ahead
             }
-            next.x = r.kbeg + (int)atomicAdd(r.work, 1u);   // the following frame, claimed ahead
         }
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-        const int4 it = s_item;
+        const int4 it = s_item[ZP ? ph : 0];
         const int k = it.x;
         if (k >= r.kend) break;
         RTL(1);
@@ -294,7 +367,24 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         // butterfly rows of this CTA, software-pipelined two deep (the loads
         // of butterfly b + 2 are issued as soon as b's registers are consumed)
         float2 x[L];
-        {
+        if constexpr (ZP) {
+            // object window and probe rows from tensor memory (zpref_store of
+            // the previous frame / the prologue)
+#pragma unroll
+            for (int b = 0; b < NPC; ++b) {
+                const int rw = q * NPC + b;
+                float2 v[Q], pv[Q];
+                tmem_ld2_f2(tmz + 2 * Q * b, v, tm + 2 * Q * b, pv);
+#pragma unroll
+                for (int s = 0; s < Q; ++s) v[s] = cmul(pv[s], v[s]);
+                dft_q<Q>(v);
+#pragma unroll
+                for (int s = 1; s < Q; ++s) v[s] = cmul(tw[rw * s], v[s]);
+#pragma unroll
+                for (int s = 0; s < Q; ++s)
+                    st_async_f2(mapa_u32(smem_u32(buf + rw * PM + t), s), v[s], mapa_u32(bar_g_u, s));
+            }
+        } else {
             const float2* zc = a.z + (size_t)pj.x * n + pj.y + t;
             float2 zb[2][Q], pb[TM ? 1 : 2][Q];   // TM: probe values read from tensor memory at use
             const size_t zstep = (size_t)L * n;
@@ -347,7 +437,16 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
             if (pass == 0 || pass == 3) {
 #pragma unroll
                 for (int kk = 0; kk < L; ++kk) x[kk] = buf[kk * PM + t];
-                if (pass == 3) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+                if (pass == 3) {
+                    if constexpr (ZP) {
+                        // the next frame's item, visible to every CTA after this barrier
+                        if (leader) {
+                            hand_item((int)(ph ^ 1u));
+                            next.x = r.kbeg + (int)atomicAdd(r.work, 1u);   // the frame after it, claimed ahead
+                        }
+                    }
+                    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+                }
             } else if (pass == 1) {
 #pragma unroll
                 for (int c = 0; c < L; c += 2) {
@@ -502,6 +601,12 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                 buf[(i * Q + s) * PM + t] = PROBE ? epi_contrib_pre(v[s], x[i * Q + s]) : epi_contrib(v[s], sc);
         }
         RTL(9);
+        // ZP: the next frame's object window, in flight across (B) and (C)
+        int4 nx = make_int4(0, 0, 0, 0);
+        if constexpr (ZP) {
+            nx = s_item[ph ^ 1u];
+            if (nx.x < r.kend) zpref_issue(nx.z, nx.w, x);
+        }
         // (B) every earlier overlapping frame has finished its update
         {
             const int d0 = __ldg(r.dep_off + k), d1 = __ldg(r.dep_off + k + 1);
@@ -577,6 +682,9 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                 }
             }
         }
+        if constexpr (ZP) {
+            if (nx.x < r.kend) zpref_store(x);
+        }
         // (D) publish: this CTA's rows of frame k are final
 #if PTG_RMW_BULK == 2
         if ((pj.y & 1) != 0) {   // (uniform) plain-store frames publish now; bulk frames once their adds complete
@@ -600,7 +708,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
         if (t < 32)
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(128u) : "memory");
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(TCOLS) : "memory");
     }
 }
 
