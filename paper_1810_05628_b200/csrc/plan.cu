@@ -390,7 +390,8 @@ void launch_rmw_t(Plan& p, const FrameArgs<float>& a, const float* amp_perm, con
     const size_t smem = cl_smem_bytes<Q, L>() + pad;
     // probe rows cached in tensor memory (frame_rmw.cuh): M = 256 probe frames
     constexpr bool TMC = PROBE && Q == 8;
-    static const bool tm_off = getenv("PTG_RMW_TMEM") && getenv("PTG_RMW_TMEM")[0] == '0';   // A/B switch
+    const char* etm = getenv("PTG_RMW_TMEM");   // A/B switch, read per launch
+    const bool tm_off = etm && etm[0] == '0';
     const bool tm = TMC && !tm_off;
     auto kern_sizing = frame_rmw_kernel<Q, L, OP, PROBE, false>;   // occupancy query (see frame_rmw.cuh)
     auto kern = tm ? frame_rmw_kernel<Q, L, OP, PROBE, TMC> : kern_sizing;

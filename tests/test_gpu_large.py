@@ -193,6 +193,47 @@ def test_rmw_matches_oracle(oracle, monkeypatch, M, steps, step, jitter, metric,
     plan.close()
 
 
+@pytest.mark.parametrize("jitter,metric", [(0, 0), (3, 0), (0, 1)])
+def test_rmw_tensor_memory_cache_bitwise(oracle, monkeypatch, jitter, metric):
+    """M = 256 RMW frames keep the probe rows and the next object window in
+    tensor memory (tcgen05.st / tcgen05.ld as thread-private storage).  With
+    PTG_RMW_TMEM=0 the same kernel reads them from L2 instead: identical
+    arithmetic, so value and gradient must agree bit for bit (odd window
+    columns through jitter, both metrics, a shift)."""
+    from paper_1810_05628_b200 import Plan, synth
+    M, steps, step = 256, 5, 48
+    n = (steps - 1) * step + M + 2 * jitter + 6
+    cfg = synth.Config(0, n, M, steps, step, 6.0, M / 4, 0.001, "c64", jitter=jitter)
+    obj, probe, pos = synth.make_inputs(cfg)
+    probe, obj = _r64(probe), _r64(obj)
+    data = oracle.simulate(n, M, M, pos, obj, probe).astype(np.float32)
+    z = _r64(obj * 0.9 + 0.05 * rand_field(n, 7))
+    v = _r64(0.01 * rand_field(n, 8))
+    monkeypatch.setenv("PTG_NO_PLANES", "1")
+    monkeypatch.setenv("PTG_RMW", "1")
+    import torch
+    plan = Plan(n, M, M, pos, data, probe, precision="c64")
+    zt = torch.from_numpy(z.astype(np.complex64)).cuda()
+    vt = torch.from_numpy(v.astype(np.complex64)).cuda()
+
+    def run():   # device buffers: plain launches (no replayed host-evaluation graph)
+        gt = torch.empty_like(zt)
+        val = plan.evaluate_device(zt, gt, vt, metric=metric)
+        return val, gt.cpu().numpy().astype(np.complex128)
+
+    on = run()
+    monkeypatch.setenv("PTG_RMW_TMEM", "0")
+    off = run()
+    monkeypatch.delenv("PTG_RMW_TMEM")
+    again = run()
+    assert on[0] == off[0] == again[0]
+    assert np.array_equal(on[1], off[1]) and np.array_equal(on[1], again[1])
+    prob = oracle.Problem(n, M, M, pos, data.astype(np.float64), probe, metric)
+    wv, wg = oracle.evaluate(prob, z, v)
+    assert rel(on[0], wv) <= C64_VAL and rel_l2(on[1], wg) <= C64_GRAD
+    plan.close()
+
+
 def test_rmw_matches_stash_path(oracle, monkeypatch):
     """Config-3 geometry: RMW and stash + gather agree (different summation
     orders of the same contributions)."""
