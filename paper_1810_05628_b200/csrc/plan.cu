@@ -23,6 +23,7 @@
 #include "frame_cl.cuh"
 #include "frame_rmw.cuh"
 #include "frame_rmw2.cuh"
+#include "frame_sc.cuh"
 #include "frame_kernels.cuh"
 #include "frame_multipass.cuh"
 #include "frame_tma.cuh"
@@ -462,6 +463,25 @@ void launch_rmw2_t(Plan& p, const FrameArgs<float>& a, const float* amp_perm, co
     PTG_CUDA(cudaLaunchKernelEx(&cfg, kern, a, amp_perm, tw, pe, r));
 }
 
+// M = 128: the four-CTA cluster fused into one persistent 512-thread CTA per SM (frame_sc.cuh)
+template <int OP, bool PROBE>
+void launch_sc_t(Plan& p, const FrameArgs<float>& a, const float* amp_perm, const float2* tw, float2* grad, int kbeg,
+                 int kend) {
+    constexpr size_t smem = sc_smem_bytes();
+    const char* etm = getenv("PTG_RMW_TMEM");   // A/B switch, read per launch
+    const bool tm = PROBE && !(etm && etm[0] == '0');
+    auto kern = tm ? frame_sc_kernel<OP, PROBE, PROBE> : frame_sc_kernel<OP, PROBE, false>;
+    set_smem_attr(kern, smem);
+    int sms = 0;
+    PTG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p.device));
+    const int grid = std::max(1, std::min(sms, kend - kbeg));
+    RmwArgs r{p.rmw_order.as<const int>(), p.rmw_dep_off.as<const int>(), p.rmw_dep_idx.as<const int>(),
+              p.rmw_done.as<unsigned>(), p.rmw_work.as<unsigned>(), grad, kbeg, kend};
+    const float2* pe = PROBE ? probe_epi_table(p, OP) : nullptr;
+    kern<<<grid, kScThreads, smem, p.stream>>>(a, amp_perm, tw, pe, r);
+    PTG_CHECK_LAUNCH();
+}
+
 // frames [kbeg, kend) of the RMW order; the dispatch counter must be zero
 template <int OP>
 void launch_rmw(Plan& p, const FrameArgs<float>& a, const float* data, float2* grad, int kbeg, int kend) {
@@ -478,7 +498,15 @@ void launch_rmw(Plan& p, const FrameArgs<float>& a, const float* data, float2* g
     // probe problem: wrong results), measures what the probe loads cost
     static const bool abl_noprobe = getenv("PTG_ABL_NOPROBE") && getenv("PTG_ABL_NOPROBE")[0] == '1';
     const bool probe = a.probe && !abl_noprobe;
-    if (p.M == 128)
+    // PTG_SC=1 (A/B, read per launch): M = 128 frames by the fused 512-thread CTA (frame_sc.cuh)
+    // instead of the four-CTA cluster -- bit-identical, measured slower (config 5's level 1, ms per
+    // evaluation: fused 5.36 / cluster RMW 4.57 / stash 4.38; with PTG_RMW_SB=256 4.33 / 4.10)
+    const char* esc = getenv("PTG_SC");
+    const bool sc = esc && esc[0] == '1';
+    if (p.M == 128 && sc)
+        probe ? launch_sc_t<OP, true>(p, a, ap, tw, grad, kbeg, kend)
+              : launch_sc_t<OP, false>(p, a, ap, tw, grad, kbeg, kend);
+    else if (p.M == 128)
         probe ? launch_rmw_t<4, 32, OP, true>(p, a, ap, tw, grad, kbeg, kend)
               : launch_rmw_t<4, 32, OP, false>(p, a, ap, tw, grad, kbeg, kend);
     else

@@ -234,6 +234,51 @@ def test_rmw_tensor_memory_cache_bitwise(oracle, monkeypatch, jitter, metric):
     plan.close()
 
 
+@pytest.mark.parametrize("steps,step,jitter,metric,tmem", [(6, 40, 0, 0, "1"), (7, 24, 2, 0, "1"), (6, 40, 0, 1, "1"),
+                                                            (7, 24, 2, 0, "0")])
+def test_fused_cta_m128_bitwise_vs_cluster(oracle, monkeypatch, steps, step, jitter, metric, tmem):
+    """M = 128 RMW frames as ONE persistent 512-thread CTA per SM (PTG_SC=1,
+    frame_sc.cuh: the four-CTA cluster fused, tensor-memory probe / window
+    cache; an A/B variant, measured slower).  Same work split and arithmetic
+    as frame_rmw_kernel<4, 32>, so value and gradient agree bit for bit; both
+    match the oracle."""
+    import torch
+
+    from paper_1810_05628_b200 import Plan, synth
+    M = 128
+    n = (steps - 1) * step + M + 2 * jitter + 6
+    cfg = synth.Config(0, n, M, steps, step, 6.0, M / 4, 0.001, "c64", jitter=jitter)
+    obj, probe, pos = synth.make_inputs(cfg)
+    probe, obj = _r64(probe), _r64(obj)
+    data = oracle.simulate(n, M, M, pos, obj, probe).astype(np.float32)
+    z = _r64(obj * 0.9 + 0.05 * rand_field(n, 7))
+    v = _r64(0.01 * rand_field(n, 8))
+    monkeypatch.setenv("PTG_NO_PLANES", "1")
+    monkeypatch.setenv("PTG_RMW", "1")
+    monkeypatch.setenv("PTG_RMW_TMEM", tmem)
+    plan = Plan(n, M, M, pos, data, probe, precision="c64")
+    zt = torch.from_numpy(z.astype(np.complex64)).cuda()
+    vt = torch.from_numpy(v.astype(np.complex64)).cuda()
+
+    def run():
+        gt = torch.empty_like(zt)
+        val = plan.evaluate_device(zt, gt, vt, metric=metric)
+        return val, gt.cpu().numpy().astype(np.complex128)
+
+    monkeypatch.setenv("PTG_SC", "1")
+    fused = run()
+    monkeypatch.setenv("PTG_SC", "0")
+    cluster = run()
+    monkeypatch.setenv("PTG_SC", "1")
+    again = run()
+    assert fused[0] == cluster[0] == again[0]
+    assert np.array_equal(fused[1], cluster[1]) and np.array_equal(fused[1], again[1])
+    prob = oracle.Problem(n, M, M, pos, data.astype(np.float64), probe, metric)
+    wv, wg = oracle.evaluate(prob, z, v)
+    assert rel(fused[0], wv) <= C64_VAL and rel_l2(fused[1], wg) <= C64_GRAD
+    plan.close()
+
+
 def test_rmw_matches_stash_path(oracle, monkeypatch):
     """Config-3 geometry: RMW and stash + gather agree (different summation
     orders of the same contributions)."""
