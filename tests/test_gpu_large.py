@@ -279,6 +279,52 @@ def test_fused_cta_m128_bitwise_vs_cluster(oracle, monkeypatch, steps, step, jit
     plan.close()
 
 
+def test_rmw_two_plans_concurrent_streams(oracle, monkeypatch):
+    """Two M = 256 RMW plans evaluated at the same time on two streams: both
+    persistent kernels want every SM's shared memory and tensor-memory columns,
+    so their clusters share the machine in whatever mix the scheduler finds.
+    The dispatch protocol (a frame is claimed only by a running cluster) and
+    the TMEM allocation must neither deadlock nor change a bit of the result."""
+    import torch
+
+    from paper_1810_05628_b200 import Plan, synth
+    M, steps, step = 256, 6, 48
+    n = (steps - 1) * step + M + 12
+    monkeypatch.setenv("PTG_NO_PLANES", "1")
+    monkeypatch.setenv("PTG_RMW", "1")
+    plans, zs, streams, want = [], [], [], []
+    for seed in (7, 9):
+        cfg = synth.Config(0, n, M, steps, step, 6.0, M / 4, 0.001, "c64", jitter=3 if seed == 9 else 0)
+        obj, probe, pos = synth.make_inputs(cfg)
+        probe, obj = _r64(probe), _r64(obj)
+        data = oracle.simulate(n, M, M, pos, obj, probe).astype(np.float32)
+        z = _r64(obj * 0.9 + 0.05 * rand_field(n, seed))
+        plan = Plan(n, M, M, pos, data, probe, precision="c64")
+        st = torch.cuda.Stream()
+        plan.set_stream(st.cuda_stream)
+        zt = torch.from_numpy(z.astype(np.complex64)).cuda()
+        gt = torch.empty_like(zt)
+        torch.cuda.synchronize()
+        val = plan.evaluate_device(zt, gt)          # alone
+        want.append((val, gt.cpu().numpy().copy()))
+        plans.append(plan)
+        zs.append(zt)
+        streams.append(st)
+    for _ in range(3):
+        outs = [torch.empty_like(zs[0]), torch.empty_like(zs[1])]
+        vals = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(2)]
+        torch.cuda.synchronize()
+        for i in (0, 1):                            # both enqueued before either finishes
+            for _ in range(4):
+                plans[i].evaluate_device(zs[i], outs[i], value_dev=vals[i], sync_value=False)
+        torch.cuda.synchronize()
+        for i in (0, 1):
+            assert float(vals[i].cpu()[0]) == want[i][0]
+            assert np.array_equal(outs[i].cpu().numpy(), want[i][1])
+    for p in plans:
+        p.close()
+
+
 def test_rmw_matches_stash_path(oracle, monkeypatch):
     """Config-3 geometry: RMW and stash + gather agree (different summation
     orders of the same contributions)."""
