@@ -171,6 +171,15 @@ __device__ __forceinline__ void tmem_ld2_f2(uint32_t ta, float2* va, uint32_t tb
 #define PTG_RMW_ZPREF 1
 #endif
 
+// PTG_ABL_NOROWSYNC (timing ablation only, wrong results): the four CTA-wide
+// barriers of the row phases replaced by __syncwarp -- an upper bound on what
+// warp-local row transforms could save
+#ifdef PTG_ABL_NOROWSYNC
+#define ROWSYNC() __syncwarp()
+#else
+#define ROWSYNC() __syncthreads()
+#endif
+
 #ifdef ABL_TIMELINE   // diagnostic build: per-frame phase stamps of the first 64 CTAs (tools/rmw_timeline.py)
 constexpr int kRtlCtas = 64, kRtlFrames = 128, kRtlStamps = 12;
 __device__ unsigned long long g_rmw_tl[kRtlCtas * kRtlFrames * kRtlStamps];
@@ -462,7 +471,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
             if (pass == 0) {
 #pragma unroll
                 for (int kk = 0; kk < L; ++kk) buf[kk * PM + t] = x[kk];
-                __syncthreads();
+                ROWSYNC();
 #pragma unroll 2
                 for (int i = 0; i < NPC; ++i) {
                     float2* row = buf + (g + Q * i) * PM + m;
@@ -475,7 +484,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
 #pragma unroll
                     for (int s = 0; s < Q; ++s) row[L * s] = v[s];
                 }
-                __syncthreads();
+                ROWSYNC();
             } else if (pass == 1) {
                 float af[4] = {0.f, 0.f, 0.f, 0.f};
                 mbar_wait(&bar_a, ph);
@@ -516,7 +525,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                 for (int c = 0; c < L; c += 2)
                     *reinterpret_cast<float4*>(&buf[rr * PM + qq * L + c]) =
                         make_float4(x[c].x, x[c].y, x[c + 1].x, x[c + 1].y);
-                __syncthreads();
+                ROWSYNC();
 #pragma unroll 2
                 for (int i = 0; i < NPC; ++i) {
                     float2* row = buf + (g + Q * i) * PM + m;
@@ -529,7 +538,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
 #pragma unroll
                     for (int s = 0; s < Q; ++s) row[L * s] = v[s];
                 }
-                __syncthreads();
+                ROWSYNC();
                 RTL(6);
             } else {
                 asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
