@@ -1079,7 +1079,7 @@ void build_rmw(Plan& p) {
     // more slack but scatter consecutive frames over more object rows (z and
     // gradient locality in L2), which costs more than the waits
     const char* esb = getenv("PTG_RMW_SB");
-    const int gap = std::max(1, esb ? atoi(esb) : w / 8);
+    const int gap = std::max(1, esb ? atoi(esb) : p.M == 128 ? 2 * w : w / 8);
     // row groups [s, e) of the row-sorted positions
     std::vector<std::pair<int, int>> rows_g;
     for (int s = 0; s < N;) {
@@ -1226,7 +1226,11 @@ void build_chunks(Plan& p) {
     if (const char* e = getenv("PTG_STASH_BUDGET_MB")) budget_b = std::max<size_t>(1, (size_t)atoll(e)) << 20;
     // (M = 128 keeps the stash even across chunks: config 5's level 1,
     // 27,556 x 128^2, 4.38 ms stash vs 5.04 ms RMW)
-    const bool big = p.M == 256 && (stash_bytes > budget_b || p.N >= 2000);
+    // PTG_RMW128=1 (A/B): M = 128 scans of >= 2000 positions by the RMW kernel too, with colour
+    // groups of two window heights (frames in flight: 148 clusters against 33 for M = 256)
+    const char* e128 = getenv("PTG_RMW128");
+    const bool rmw128 = e128 && e128[0] == '1';
+    const bool big = (p.M == 256 && (stash_bytes > budget_b || p.N >= 2000)) || (rmw128 && p.M == 128 && p.N >= 2000);
     p.rmw_mode = (!p.planes_mode && p.cl && p.w == p.M && p.N > 0 && !no_rmw && !budget_override_off &&
                   (force_rmw || big)) ||
                  (p.rows != p.n && p.N > 0);
