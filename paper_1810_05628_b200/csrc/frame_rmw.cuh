@@ -174,6 +174,12 @@ __device__ __forceinline__ void tmem_ld2_f2(uint32_t ta, float2* va, uint32_t tb
 // st.shared::cluster stores closed by a cluster barrier instead of st.async
 // with a complete_tx on the owner's mbarrier per store (64 K transaction
 // updates per CTA and frame): 19.78 vs 20.09 ms on config 5 (0 = st.async)
+// PTG_RMW_DFTQ_UNROLL (A/B): unroll factor of the row radix-Q loops in shared memory (NPC iterations)
+#ifndef PTG_RMW_DFTQ_UNROLL
+#define PTG_RMW_DFTQ_UNROLL 4
+#endif
+#define PTG_PRAGMA_(x) _Pragma(#x)
+#define PTG_UNROLL_N(n) PTG_PRAGMA_(unroll n)
 #ifndef PTG_RMW_GATHER_PLAIN
 #define PTG_RMW_GATHER_PLAIN 1
 #endif
@@ -493,7 +499,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
 #pragma unroll
                 for (int kk = 0; kk < L; ++kk) buf[kk * PM + t] = x[kk];
                 ROWSYNC();
-#pragma unroll 2
+PTG_UNROLL_N(PTG_RMW_DFTQ_UNROLL)
                 for (int i = 0; i < NPC; ++i) {
                     float2* row = buf + (g + Q * i) * PM + m;
                     float2 v[Q];
@@ -547,7 +553,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                     *reinterpret_cast<float4*>(&buf[rr * PM + qq * L + c]) =
                         make_float4(x[c].x, x[c].y, x[c + 1].x, x[c + 1].y);
                 ROWSYNC();
-#pragma unroll 2
+PTG_UNROLL_N(PTG_RMW_DFTQ_UNROLL)
                 for (int i = 0; i < NPC; ++i) {
                     float2* row = buf + (g + Q * i) * PM + m;
                     float2 v[Q];
