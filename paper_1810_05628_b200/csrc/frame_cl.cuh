@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
     for (int s = 0; s < Q; ++s) rtw[s] = tw[m * s];
     const float* A = amp_perm + (size_t)j * M * M + ((size_t)q * L + rr) * M + (size_t)qq * L;
     double acc = 0.0;
-#pragma unroll 1
+PTG_UNROLL_N(PTG_CL_PASS_UNROLL)
     for (int pass = 0; pass < 4; ++pass) {
         if (pass == 0 || pass == 3) {   // column t of the local rows
 #pragma unroll

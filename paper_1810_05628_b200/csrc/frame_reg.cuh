@@ -26,6 +26,26 @@
 #include "frame_kernels.cuh"
 #include <utility>
 
+// unroll factor as a macro argument (A/B variants of the pass loops)
+#define PTG_PRAGMA_(x) _Pragma(#x)
+#define PTG_UNROLL_N(n) PTG_PRAGMA_(unroll n)
+// the four register-FFT passes of a frame kernel: 1 = one rolled loop (one
+// copy of the body), 4 = unrolled (each pass specialised, the next pass's
+// loads scheduled across the boundary).  Measured per kernel (round 2):
+//   PTG_RMW_PASS_UNROLL (frame_rmw / frame_sc)  config 5   19.66 -> 18.84 ms  => 4
+//   PTG_CL_PASS_UNROLL  (frame_cl)              config 3   0.1598 -> 0.1504 ms => 4
+//   PTG_TMA_PASS_UNROLL (frame_tma)             config 2   0.0279 -> 0.0280 ms (254 registers) => 1
+//   PTG_PIE_PASS_UNROLL (pie_reg)               PIE sweep  5.19 -> 6.48 ms => 1
+#ifndef PTG_CL_PASS_UNROLL
+#define PTG_CL_PASS_UNROLL 4
+#endif
+#ifndef PTG_TMA_PASS_UNROLL
+#define PTG_TMA_PASS_UNROLL 1
+#endif
+#ifndef PTG_PIE_PASS_UNROLL
+#define PTG_PIE_PASS_UNROLL 1
+#endif
+
 namespace ptg {
 
 #ifdef ABL_TIMELINE   // diagnostic build: per-CTA globaltimer stamps (tools/timeline.py)

@@ -178,8 +178,12 @@ __device__ __forceinline__ void tmem_ld2_f2(uint32_t ta, float2* va, uint32_t tb
 #ifndef PTG_RMW_DFTQ_UNROLL
 #define PTG_RMW_DFTQ_UNROLL 4
 #endif
-#define PTG_PRAGMA_(x) _Pragma(#x)
-#define PTG_UNROLL_N(n) PTG_PRAGMA_(unroll n)
+// PTG_RMW_PASS_UNROLL: 4 (default) = the four FFT_L passes unrolled (each pass
+// specialised, loads of the next pass scheduled across the boundary: config 5
+// 19.66 -> 18.84 ms, 3,576 -> 4,416 SASS instructions); 1 = one rolled loop
+#ifndef PTG_RMW_PASS_UNROLL
+#define PTG_RMW_PASS_UNROLL 4
+#endif
 #ifndef PTG_RMW_GATHER_PLAIN
 #define PTG_RMW_GATHER_PLAIN 1
 #endif
@@ -468,7 +472,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
         RTL(3);
 
         double acc = 0.0;
-#pragma unroll 1
+PTG_UNROLL_N(PTG_RMW_PASS_UNROLL)
         for (int pass = 0; pass < 4; ++pass) {
             if (pass == 0 || pass == 3) {
 #pragma unroll

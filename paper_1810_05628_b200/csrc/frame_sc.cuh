@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kScThreads, 1)
         __syncthreads();   // every group's rows have landed
 
         double acc = 0.0;
-#pragma unroll 1
+PTG_UNROLL_N(PTG_RMW_PASS_UNROLL)
         for (int pass = 0; pass < 4; ++pass) {
             if (pass == 0 || pass == 3) {
 #pragma unroll

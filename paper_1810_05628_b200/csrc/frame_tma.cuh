@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(M * tma_frames_per_cta<M>(), M == 64 ? 6 : 3)
 
     const float* amp_tile = reinterpret_cast<const float*>(fr);
     double acc = 0.0;
-#pragma unroll 1
+PTG_UNROLL_N(PTG_TMA_PASS_UNROLL)
     for (int pass = 0; pass < 4; ++pass) {
         reg_fft<M, false>(x);
         if (pass == 1) TL(2);

@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(M, 1)
             zw[r * M + t] = x[r];
             x[r] = cmul(P[r * M + t], x[r]);
         }
-#pragma unroll 1
+PTG_UNROLL_N(PTG_PIE_PASS_UNROLL)
         for (int pass = 0; pass < 4; ++pass) {
             reg_fft<M, false>(x);
             if (pass == 0 || pass == 2) {   // transpose through shared memory
