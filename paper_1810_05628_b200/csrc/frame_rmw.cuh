@@ -184,6 +184,16 @@ __device__ __forceinline__ void tmem_ld2_f2(uint32_t ta, float2* va, uint32_t tb
 #ifndef PTG_RMW_PASS_UNROLL
 #define PTG_RMW_PASS_UNROLL 4
 #endif
+// PTG_RMW_LATE_SIGNALS=1 (default, tensor-memory path; config 5 18.78 ->
+// 18.29 ms): a .release arrival first waits
+// for every outstanding memory operation of its thread, so a long-latency
+// operation issued just before one stalls the whole cluster.  The leader's
+// claim atomic moves behind the inverse pass's arrival, and the publish of
+// frame k (red.release.gpu) behind the NEXT loop-top arrival: both L2 round
+// trips then overlap the barrier instead of preceding it.
+#ifndef PTG_RMW_LATE_SIGNALS
+#define PTG_RMW_LATE_SIGNALS 1
+#endif
 #ifndef PTG_RMW_GATHER_PLAIN
 #define PTG_RMW_GATHER_PLAIN 1
 #endif
@@ -356,6 +366,8 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
 #ifdef ABL_TIMELINE
     int rtl_f = 0;
 #endif
+    constexpr bool LATE = ZP && PTG_RMW_LATE_SIGNALS != 0 && PTG_RMW_BULK != 2;
+    int pub_k = -1;   // LATE: frame whose rows are final but not yet published (thread 0)
 #pragma unroll 1
     for (;;) {
         RTL(0);
@@ -373,6 +385,9 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
             }
         }
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        if constexpr (LATE) {
+            if (t == 0 && pub_k >= 0) red_release_gpu_add(r.done + pub_k, 1u);
+        }
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         const int4 it = s_item[ZP ? ph : 0];
         const int k = it.x;
@@ -454,7 +469,10 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                     st_async_f2(mapa_u32(smem_u32(buf + rw * PM + t), s), v[s], mapa_u32(bar_g_u, s));
             }
         }
-        if (leader && next.x < r.kend) next.y = __ldg(r.order + next.x);
+        constexpr bool ORDER_LATE = LATE && PTG_RMW_GATHER_PLAIN != 0;   // the leader's load behind the arrival below
+        if constexpr (!ORDER_LATE) {
+            if (leader && next.x < r.kend) next.y = __ldg(r.order + next.x);
+        }
         RTL(2);
 #if PTG_RMW_BULK == 2
         publish_pending();   // the previous frame's reduce-adds landed during this gather
@@ -462,6 +480,9 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
 #if PTG_RMW_GATHER_PLAIN
         if constexpr (ZP) {
             asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+            if constexpr (ORDER_LATE) {
+                if (leader && next.x < r.kend) next.y = __ldg(r.order + next.x);
+            }
             asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         } else {
             mbar_wait(&bar_g, ph);
@@ -482,10 +503,13 @@ PTG_UNROLL_N(PTG_RMW_PASS_UNROLL)
                         // the next frame's item, visible to every CTA after this barrier
                         if (leader) {
                             hand_item((int)(ph ^ 1u));
-                            next.x = r.kbeg + (int)atomicAdd(r.work, 1u);   // the frame after it, claimed ahead
+                            if constexpr (!LATE) next.x = r.kbeg + (int)atomicAdd(r.work, 1u);   // the frame after it, claimed ahead
                         }
                     }
                     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+                    if constexpr (LATE) {
+                        if (leader) next.x = r.kbeg + (int)atomicAdd(r.work, 1u);
+                    }
                 }
             } else if (pass == 1) {
 #pragma unroll
@@ -733,7 +757,8 @@ PTG_UNROLL_N(PTG_RMW_DFTQ_UNROLL)
         }
 #else
         __syncthreads();
-        if (t == 0) red_release_gpu_add(r.done + k, 1u);
+        if constexpr (LATE) pub_k = k;
+        else if (t == 0) red_release_gpu_add(r.done + k, 1u);
 #endif
         RTL(11);
 #ifdef ABL_TIMELINE
