@@ -176,10 +176,6 @@ __device__ __forceinline__ void tmem_ld2_f2(uint32_t ta, float2* va, uint32_t tb
 #ifndef PTG_RMW_ZPREF
 #define PTG_RMW_ZPREF 1
 #endif
-// PTG_RMW_GATHER_PLAIN=1 (default, ZP path): the gather's pushes as plain
-// st.shared::cluster stores closed by a cluster barrier instead of st.async
-// with a complete_tx on the owner's mbarrier per store (64 K transaction
-// updates per CTA and frame): 19.78 vs 20.09 ms on config 5 (0 = st.async)
 // PTG_RMW_DFTQ_UNROLL (A/B): unroll factor of the row radix-Q loops in shared memory (NPC iterations)
 #ifndef PTG_RMW_DFTQ_UNROLL
 #define PTG_RMW_DFTQ_UNROLL 4
@@ -191,8 +187,8 @@ __device__ __forceinline__ void tmem_ld2_f2(uint32_t ta, float2* va, uint32_t tb
 #define PTG_RMW_PASS_UNROLL 4
 #endif
 // PTG_RMW_LATE_SIGNALS=1 (default, tensor-memory path; config 5 18.78 ->
-// 18.29 ms): a .release arrival first waits
-// for every outstanding memory operation of its thread, so a long-latency
+// 18.29 ms): a .release arrival first waits for every outstanding memory
+// operation of its thread, so a long-latency
 // operation issued just before one stalls the whole cluster.  The leader's
 // claim atomic moves behind the inverse pass's arrival, and the publish of
 // frame k (red.release.gpu) behind the NEXT loop-top arrival: both L2 round
@@ -214,6 +210,10 @@ __device__ __forceinline__ void tmem_ld2_f2(uint32_t ta, float2* va, uint32_t tb
 #ifndef PTG_RMW_EARLY_DEPS
 #define PTG_RMW_EARLY_DEPS 1
 #endif
+// PTG_RMW_GATHER_PLAIN=1 (default, ZP path): the gather's pushes as plain
+// st.shared::cluster stores closed by a cluster barrier instead of st.async
+// with a complete_tx on the owner's mbarrier per store (64 K transaction
+// updates per CTA and frame): 19.78 vs 20.09 ms on config 5 (0 = st.async)
 #ifndef PTG_RMW_GATHER_PLAIN
 #define PTG_RMW_GATHER_PLAIN 1
 #endif
