@@ -207,6 +207,13 @@ __device__ __forceinline__ void tmem_ld2_f2(uint32_t ta, float2* va, uint32_t tb
 // issued in stages through the frame -- bounds at the frame start, the entry
 // behind the post-gather arrival, the acquire load before the contributions --
 // so that (B) usually finds its answer already in a register
+// PTG_RMW_STAGGER=1 (default; 18.16 -> 17.75 ms): odd cluster ranks push to
+// owners 4..7 first, even ranks to owners 0..3 first, so the Q sources do not
+// all address the same owner at once.  2 = rank q starts at owner q (a branch
+// per rank): 18.12, no better than unstaggered.
+#ifndef PTG_RMW_STAGGER
+#define PTG_RMW_STAGGER 1
+#endif
 #ifndef PTG_RMW_EARLY_DEPS
 #define PTG_RMW_EARLY_DEPS 1
 #endif
@@ -456,6 +463,32 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                 dft_q<Q>(v);
 #pragma unroll
                 for (int s = 1; s < Q; ++s) v[s] = cmul(tw[rw * s], v[s]);
+#if PTG_RMW_STAGGER && PTG_RMW_GATHER_PLAIN
+#if PTG_RMW_STAGGER == 2
+                // rank q starts at owner q: at every step the Q sources address Q different owners
+#pragma unroll
+                for (int R = 0; R < Q; ++R)
+                    if (q == R) {
+#pragma unroll
+                        for (int s2 = 0; s2 < Q; ++s2) {
+                            const int s = (s2 + R) % Q;
+                            st_cluster_f2(mapa_u32(smem_u32(buf + rw * PM + t), s), v[s]);
+                        }
+                    }
+#else
+                if (q & 1) {
+#pragma unroll
+                    for (int s2 = 0; s2 < Q; ++s2) {
+                        constexpr int H = Q / 2;
+                        const int s = (s2 + H) % Q;
+                        st_cluster_f2(mapa_u32(smem_u32(buf + rw * PM + t), s), v[s]);
+                    }
+                } else {
+#pragma unroll
+                    for (int s = 0; s < Q; ++s) st_cluster_f2(mapa_u32(smem_u32(buf + rw * PM + t), s), v[s]);
+                }
+#endif
+#else
 #pragma unroll
                 for (int s = 0; s < Q; ++s) {
 #if PTG_RMW_GATHER_PLAIN
@@ -464,6 +497,7 @@ __global__ void __launch_bounds__(Q * L, cl_min_blocks<Q, L>())
                     st_async_f2(mapa_u32(smem_u32(buf + rw * PM + t), s), v[s], mapa_u32(bar_g_u, s));
 #endif
                 }
+#endif
             }
         } else {
             const float2* zc = a.z + (size_t)pj.x * n + pj.y + t;
@@ -643,6 +677,32 @@ PTG_UNROLL_N(PTG_RMW_DFTQ_UNROLL)
                                          kk / NPC),
                                 x[kk], mapa_u32(bar_p_u, kk / NPC));
 #else
+#if PTG_RMW_STAGGER == 2
+                if (true) {
+#pragma unroll
+                    for (int R = 0; R < Q; ++R)
+                        if (q == R) {
+#pragma unroll
+                            for (int k2 = 0; k2 < L; ++k2) {
+                                const int kk = (k2 + R * NPC) % L;
+                                st_cluster_f2(
+                                    mapa_u32(buf_u + (uint32_t)((((kk % NPC) * Q + q) * PM + t) * sizeof(float2)),
+                                             kk / NPC),
+                                    x[kk]);
+                            }
+                        }
+                } else
+#elif PTG_RMW_STAGGER
+                if (q & 1) {
+#pragma unroll
+                    for (int k2 = 0; k2 < L; ++k2) {
+                        const int kk = (k2 + L / 2) % L;
+                        st_cluster_f2(mapa_u32(buf_u + (uint32_t)((((kk % NPC) * Q + q) * PM + t) * sizeof(float2)),
+                                               kk / NPC),
+                                      x[kk]);
+                    }
+                } else
+#endif
 #pragma unroll
                 for (int kk = 0; kk < L; ++kk)   // remote row (kk % NPC) Q + q of CTA kk / NPC
                     st_cluster_f2(mapa_u32(buf_u + (uint32_t)((((kk % NPC) * Q + q) * PM + t) * sizeof(float2)),
